@@ -1,0 +1,1049 @@
+// kmeans_engine.cu — host engine + C ABI (include/kmeans_b200.h).
+//
+// The engine owns one CUDA stream on one device, the resident point matrix and
+// the per-k device buffers.  km_lloyd reproduces engine.iterate
+// (/root/reference/pkg/src/kmeans_regimes/engine.py:320-343) with the loop
+// control on the device: every kernel checks the device-side DevState and the
+// host reads that state once per batch of iterations (one 48-byte D2H).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kmeans_b200.h"
+#include "kmeans_kernels.cuh"
+
+using namespace km;
+
+static thread_local std::string g_global_err;
+
+struct km_engine {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  size_t smem_optin = 227 * 1024;
+  std::string err;
+
+  // resident points
+  void* x = nullptr;
+  bool x_owned = false;
+  int64_t n = 0;
+  int32_t m = 0;
+  int32_t point_bytes = 4;
+  double absmax = 0.0;
+  int32_t frac_bits = 0;
+  bool frac_user = false;
+
+  // per-k buffers
+  int32_t k = 0;
+  int32_t mpad = 0;
+  int32_t* labels = nullptr;        // n
+  unsigned long long* part = nullptr;  // k*m + k
+  double* cur = nullptr;            // k*m
+  double* prev = nullptr;           // k*m
+  long long* model_counts = nullptr;  // k
+  float* w = nullptr;               // k*mpad
+  float* cn = nullptr;              // k
+  float* cmax = nullptr;            // 1
+  DevState* st = nullptr;           // device
+  DevState* st_host = nullptr;      // pinned
+  double* d2 = nullptr;             // n (repair, lazily)
+  ArgMax* partials = nullptr;       // argmax partials
+  ArgMax* winner = nullptr;         // 1
+  int32_t* scratch_i = nullptr;     // small device scratch
+  double* scratch_d = nullptr;      // 2*k*m device scratch
+  unsigned long long* scratch_u = nullptr;  // 2
+  long long* labels64 = nullptr;    // n (download staging)
+  int n_partials = 0;
+
+  km_stats stats{};
+  bool profiling = false;
+  std::vector<cudaEvent_t> ev;  // profiling event pool (pairs)
+};
+
+// ---------------------------------------------------------------------------
+// error plumbing
+// ---------------------------------------------------------------------------
+static int set_err(km_engine* e, int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (e) e->err = buf; else g_global_err = buf;
+  return code;
+}
+
+static int cuda_fail(km_engine* e, cudaError_t c, const char* what) {
+  const int code = (c == cudaErrorMemoryAllocation) ? KM_ERR_CAPACITY
+                   : (c == cudaErrorNoDevice || c == cudaErrorInsufficientDriver || c == cudaErrorInvalidDevice)
+                       ? KM_ERR_DEVICE_UNAVAILABLE
+                       : KM_ERR_DEVICE_LOST;
+  cudaGetLastError();  // clear sticky-free errors
+  return set_err(e, code, "%s: %s (%s)", what, cudaGetErrorString(c), cudaGetErrorName(c));
+}
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t _c = (call);                              \
+    if (_c != cudaSuccess) return cuda_fail(e, _c, #call); \
+  } while (0)
+
+#define CK_LAUNCH(what)                                   \
+  do {                                                    \
+    cudaError_t _c = cudaGetLastError();                  \
+    if (_c != cudaSuccess) return cuda_fail(e, _c, what); \
+  } while (0)
+
+template <typename P>
+static int dalloc(km_engine* e, P** p, size_t bytes) {
+  if (*p) { cudaFree(*p); *p = nullptr; }
+  if (bytes == 0) bytes = 16;
+  cudaError_t c = cudaMalloc((void**)p, bytes);
+  if (c != cudaSuccess) { *p = nullptr; return cuda_fail(e, c, "cudaMalloc"); }
+  return KM_OK;
+}
+
+static void dfree(void* p) { if (p) cudaFree(p); }
+
+// ---------------------------------------------------------------------------
+// launch helpers
+// ---------------------------------------------------------------------------
+static int mp_for(int m) {
+  static const int mps[] = {4, 8, 12, 16, 20, 24, 28, 32, 40, 48, 64};
+  for (int v : mps) if (m <= v) return v;
+  return 0;  // generic
+}
+
+static size_t pass_smem_bytes(const km_engine* e, bool assign, bool smem_acc, int elem_bytes) {
+  size_t b = 0;
+  if (smem_acc) b += ((size_t)e->k * e->m + e->k) * 8;
+  if (assign) b += (size_t)e->k * e->mpad * 4 + (size_t)e->k * 4;
+  b = (b + 15) & ~size_t(15);
+  b += (size_t)kTileRows * e->m * elem_bytes;
+  return b;
+}
+
+template <typename T, int MP, bool A, bool S, bool SA>
+static int launch_pass_t(km_engine* e, const PassArgs& a, size_t smem) {
+  auto kern = lloyd_pass_kernel<T, MP, A, S, SA>;
+  if (smem > 48 * 1024) {
+    cudaError_t c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (c != cudaSuccess) return cuda_fail(e, c, "cudaFuncSetAttribute(pass smem)");
+  }
+  int per_sm = 0;
+  cudaError_t c = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (c != cudaSuccess) return cuda_fail(e, c, "occupancy");
+  if (per_sm < 1) return set_err(e, KM_ERR_CAPACITY, "pass kernel does not fit on an SM (smem %zu B)", smem);
+  const int64_t ntiles = (a.n + kTileRows - 1) / kTileRows;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * e->num_sms));
+  kern<<<(unsigned)grid, kThreads, smem, e->stream>>>(a);
+  CK_LAUNCH("lloyd_pass_kernel launch");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
+template <typename T, bool A, bool S, bool SA>
+static int launch_pass_mp(km_engine* e, const PassArgs& a, size_t smem) {
+  if (!A) return launch_pass_t<T, 0, A, S, SA>(e, a, smem);
+  switch (mp_for(e->m)) {
+    case 4: return launch_pass_t<T, 4, A, S, SA>(e, a, smem);
+    case 8: return launch_pass_t<T, 8, A, S, SA>(e, a, smem);
+    case 12: return launch_pass_t<T, 12, A, S, SA>(e, a, smem);
+    case 16: return launch_pass_t<T, 16, A, S, SA>(e, a, smem);
+    case 20: return launch_pass_t<T, 20, A, S, SA>(e, a, smem);
+    case 24: return launch_pass_t<T, 24, A, S, SA>(e, a, smem);
+    case 28: return launch_pass_t<T, 28, A, S, SA>(e, a, smem);
+    case 32: return launch_pass_t<T, 32, A, S, SA>(e, a, smem);
+    case 40: return launch_pass_t<T, 40, A, S, SA>(e, a, smem);
+    case 48: return launch_pass_t<T, 48, A, S, SA>(e, a, smem);
+    case 64: return launch_pass_t<T, 64, A, S, SA>(e, a, smem);
+    default: return launch_pass_t<T, 0, A, S, SA>(e, a, smem);
+  }
+}
+
+enum PassMode { PASS_ASSIGN_SUMS = 0, PASS_ASSIGN_ONLY = 1, PASS_SUMS_ONLY = 2 };
+
+static float host_err_coef(int m) { return (float)((m + 8) * std::ldexp(1.0, -24) * 1.25); }
+
+static int launch_pass(km_engine* e, PassMode mode, bool gated) {
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  const bool A = mode != PASS_SUMS_ONLY;
+  PassArgs a{};
+  a.x = e->x;
+  a.n = e->n;
+  a.m = e->m;
+  a.k = e->k;
+  a.w = e->w;
+  a.cn = e->cn;
+  a.cmax = e->cmax;
+  a.c64 = e->cur;
+  a.labels = e->labels;
+  a.part = e->part;
+  const int F = e->frac_bits;
+  a.scale_d = std::ldexp(1.0, F);
+  a.use_dscale = (F > 120 || F < -120) ? 1 : 0;
+  a.scale_f = a.use_dscale ? 1.0f : (float)std::ldexp(1.0, F);
+  a.mpad = e->mpad;
+  a.err_coef = host_err_coef(e->m);
+  a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -140));
+  a.nx_inflate = (float)(1.0 + (e->m + 2) * std::ldexp(1.0, -24));
+  const bool huge = e->absmax > std::ldexp(1.0, 50);
+  const bool tiny64 = e->point_bytes == 8 && e->absmax > 0 && e->absmax < std::ldexp(1.0, -100);
+  a.exact_only = (huge || tiny64) ? 1 : 0;
+  a.st = e->st;
+  a.gate = gated ? 1 : 0;
+  const PassArgs& a2 = a;
+  const int eb = e->point_bytes;
+  size_t smem_sa = pass_smem_bytes(e, A, true, eb);
+  const bool sa = smem_sa <= e->smem_optin;
+  size_t smem = sa ? smem_sa : pass_smem_bytes(e, A, false, eb);
+  if (smem > e->smem_optin)
+    return set_err(e, KM_ERR_CAPACITY, "k=%d, m=%d needs %zu B of shared memory per CTA (max %zu)", e->k, e->m, smem,
+                   e->smem_optin);
+  if (eb == 4) {
+    if (mode == PASS_ASSIGN_SUMS) return sa ? launch_pass_mp<float, true, true, true>(e, a2, smem) : launch_pass_mp<float, true, true, false>(e, a2, smem);
+    if (mode == PASS_ASSIGN_ONLY) return sa ? launch_pass_mp<float, true, false, true>(e, a2, smem) : launch_pass_mp<float, true, false, false>(e, a2, smem);
+    return sa ? launch_pass_mp<float, false, true, true>(e, a2, smem) : launch_pass_mp<float, false, true, false>(e, a2, smem);
+  } else {
+    if (mode == PASS_ASSIGN_SUMS) return sa ? launch_pass_mp<double, true, true, true>(e, a2, smem) : launch_pass_mp<double, true, true, false>(e, a2, smem);
+    if (mode == PASS_ASSIGN_ONLY) return sa ? launch_pass_mp<double, true, false, true>(e, a2, smem) : launch_pass_mp<double, true, false, false>(e, a2, smem);
+    return sa ? launch_pass_mp<double, false, true, true>(e, a2, smem) : launch_pass_mp<double, false, true, false>(e, a2, smem);
+  }
+}
+
+static FinishArgs finish_args(km_engine* e, int mode) {
+  FinishArgs f{};
+  f.part = e->part;
+  f.cur = e->cur;
+  f.prev = e->prev;
+  f.model_counts = e->model_counts;
+  f.w = e->w;
+  f.cn = e->cn;
+  f.cmax = e->cmax;
+  f.k = e->k;
+  f.m = e->m;
+  f.mpad = e->mpad;
+  f.inv_scale = std::ldexp(1.0, -e->frac_bits);
+  f.st = e->st;
+  f.mode = mode;
+  return f;
+}
+
+static int finish_threads(int k, int m) {
+  const int work = std::max(k, k * m);
+  int t = 128;
+  while (t < 512 && t < work) t *= 2;
+  return t;
+}
+
+static int launch_finish(km_engine* e, int mode) {
+  FinishArgs f = finish_args(e, mode);
+  lloyd_finish_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(f);
+  CK_LAUNCH("lloyd_finish_kernel launch");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
+static int launch_check(km_engine* e) {
+  FinishArgs f = finish_args(e, 0);
+  lloyd_check_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(f);
+  CK_LAUNCH("lloyd_check_kernel launch");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
+static int launch_prep(km_engine* e) {
+  prep_filter_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(e->cur, e->w, e->cn, e->cmax, e->k, e->m,
+                                                                      e->mpad);
+  CK_LAUNCH("prep_filter_kernel launch");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
+static int read_state(km_engine* e) {
+  CK(cudaMemcpyAsync(e->st_host, e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  e->stats.host_syncs += 1;
+  return KM_OK;
+}
+
+static int reset_state(km_engine* e, int max_iters, double tol) {
+  DevState s{};
+  s.max_iters = max_iters;
+  s.tol = tol;
+  *e->st_host = s;
+  CK(cudaMemcpyAsync(e->st, e->st_host, sizeof(DevState), cudaMemcpyHostToDevice, e->stream));
+  return KM_OK;
+}
+
+static int grid_for(km_engine* e, int64_t n, int per_sm = 8) {
+  int64_t g = (n + 255) / 256;
+  g = std::min<int64_t>(g, (int64_t)e->num_sms * per_sm);
+  return (int)std::max<int64_t>(1, g);
+}
+
+// ---------------------------------------------------------------------------
+// buffers
+// ---------------------------------------------------------------------------
+static void free_k(km_engine* e) {
+  dfree(e->labels); dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
+  dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->d2); dfree(e->partials); dfree(e->winner);
+  dfree(e->scratch_d); dfree(e->labels64);
+  e->labels = nullptr; e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
+  e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->d2 = nullptr; e->partials = nullptr; e->winner = nullptr;
+  e->scratch_d = nullptr; e->labels64 = nullptr;
+  e->k = 0;
+}
+
+static int ensure_k(km_engine* e, int32_t k) {
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (k < 1) return set_err(e, KM_ERR_CONTRACT, "k must be >= 1, got %d", k);
+  if (k == e->k && e->labels) return KM_OK;
+  free_k(e);
+  const int m = e->m;
+  e->mpad = mp_for(m) ? mp_for(m) : ((m + 3) & ~3);
+  int r;
+  if ((r = dalloc(e, &e->labels, sizeof(int32_t) * (size_t)e->n))) return r;
+  if ((r = dalloc(e, &e->part, 8 * ((size_t)k * m + k)))) return r;
+  if ((r = dalloc(e, &e->cur, 8 * (size_t)k * m))) return r;
+  if ((r = dalloc(e, &e->prev, 8 * (size_t)k * m))) return r;
+  if ((r = dalloc(e, &e->model_counts, 8 * (size_t)k))) return r;
+  if ((r = dalloc(e, &e->w, 4 * (size_t)k * e->mpad))) return r;
+  if ((r = dalloc(e, &e->cn, 4 * (size_t)k))) return r;
+  if ((r = dalloc(e, &e->cmax, 16))) return r;
+  if ((r = dalloc(e, &e->scratch_d, 8 * 2 * (size_t)k * m))) return r;
+  e->n_partials = grid_for(e, e->n);
+  if ((r = dalloc(e, &e->partials, sizeof(ArgMax) * (size_t)e->n_partials))) return r;
+  if ((r = dalloc(e, &e->winner, sizeof(ArgMax)))) return r;
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * m + k), e->stream));
+  CK(cudaMemsetAsync(e->labels, 0, sizeof(int32_t) * (size_t)e->n, e->stream));
+  e->k = k;
+  return KM_OK;
+}
+
+static int compute_frac_bits(double absmax, int64_t n_total) {
+  if (n_total < 1) n_total = 1;
+  double bound = std::max(absmax, 1e-300) * (double)n_total;
+  int ex = 0;
+  std::frexp(bound, &ex);  // bound < 2^ex
+  int F = 62 - ex;
+  if (absmax == 0.0) F = 62 - 1 - (int)std::ceil(std::log2((double)n_total));
+  F = std::max(-60, std::min(1000, F));
+  return F;
+}
+
+// exact max |x| (+ finiteness) on the device; sets the fixed-point scale.
+static int scan_points(km_engine* e, const void* x, int bytes_per, int64_t count, int* flags_out) {
+  unsigned long long zero = 0;
+  int zf[2] = {0, 0};
+  CK(cudaMemcpyAsync(e->scratch_u, &zero, 8, cudaMemcpyHostToDevice, e->stream));
+  CK(cudaMemcpyAsync(e->scratch_i, zf, 8, cudaMemcpyHostToDevice, e->stream));
+  const int g = grid_for(e, count, 4);
+  if (bytes_per == 4)
+    absmax_kernel<float><<<g, 256, 0, e->stream>>>((const float*)x, count, e->scratch_u, e->scratch_i);
+  else
+    absmax_kernel<double><<<g, 256, 0, e->stream>>>((const double*)x, count, e->scratch_u, e->scratch_i);
+  CK_LAUNCH("absmax_kernel");
+  e->stats.kernel_launches += 1;
+  unsigned long long bits = 0;
+  CK(cudaMemcpyAsync(&bits, e->scratch_u, 8, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaMemcpyAsync(flags_out, e->scratch_i, 8, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  double v;
+  std::memcpy(&v, &bits, 8);
+  e->absmax = v;
+  return KM_OK;
+}
+
+static int after_points_loaded(km_engine* e) {
+  if (!e->frac_user) e->frac_bits = compute_frac_bits(e->absmax, e->n);
+  e->stats.frac_bits = e->frac_bits;
+  e->stats.point_bytes = e->point_bytes;
+  return KM_OK;
+}
+
+static int drop_points(km_engine* e) {
+  free_k(e);
+  if (e->x && e->x_owned) cudaFree(e->x);
+  e->x = nullptr;
+  e->x_owned = false;
+  e->n = 0;
+  e->m = 0;
+  return KM_OK;
+}
+
+static int validate_points_shape(km_engine* e, const void* x, int64_t n, int32_t m) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!x) return set_err(e, KM_ERR_CONTRACT, "null point buffer");
+  if (n < 1 || m < 1) return set_err(e, KM_ERR_CONTRACT, "points must be non-empty, got shape (%lld, %d)", (long long)n, m);
+  if (n > (int64_t)INT32_MAX * 64) return set_err(e, KM_ERR_CONTRACT, "n too large");
+  return KM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// repair (engine.py:265-276), single shard
+// ---------------------------------------------------------------------------
+static int self_d2(km_engine* e) {
+  if (!e->d2) { int r = dalloc(e, &e->d2, 8 * (size_t)e->n); if (r) return r; }
+  const int g = grid_for(e, e->n);
+  if (e->point_bytes == 4)
+    self_d2_kernel<float><<<g, 256, 0, e->stream>>>((const float*)e->x, e->n, e->m, e->cur, e->labels, e->d2);
+  else
+    self_d2_kernel<double><<<g, 256, 0, e->stream>>>((const double*)e->x, e->n, e->m, e->cur, e->labels, e->d2);
+  CK_LAUNCH("self_d2_kernel");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
+static int empty_list(km_engine* e, std::vector<int32_t>& out) {
+  std::vector<long long> cnt(e->k);
+  CK(cudaMemcpyAsync(cnt.data(), e->model_counts, 8 * (size_t)e->k, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  out.clear();
+  for (int c = 0; c < e->k; ++c) if (cnt[c] == 0) out.push_back(c);
+  return KM_OK;
+}
+
+static int repair_local(km_engine* e) {
+  std::vector<int32_t> empties;
+  int r;
+  if ((r = empty_list(e, empties))) return r;
+  if (empties.empty()) return KM_OK;
+  if ((r = self_d2(e))) return r;
+  for (int32_t c : empties) {
+    argmax_partial_kernel<<<e->n_partials, 256, 0, e->stream>>>(e->d2, e->n, e->partials);
+    CK_LAUNCH("argmax_partial_kernel");
+    if (e->point_bytes == 4)
+      repair_apply_kernel<float><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const float*)e->x, e->m,
+                                                          e->labels, e->d2, e->model_counts, e->cur, e->winner);
+    else
+      repair_apply_kernel<double><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const double*)e->x, e->m,
+                                                           e->labels, e->d2, e->model_counts, e->cur, e->winner);
+    CK_LAUNCH("repair_apply_kernel");
+    e->stats.repairs += 1;
+    e->stats.kernel_launches += 2;
+  }
+  return KM_OK;
+}
+
+static int download_labels(km_engine* e, int64_t* out) {
+  if (!e->labels64) { int r = dalloc(e, &e->labels64, 8 * (size_t)e->n); if (r) return r; }
+  widen_labels_kernel<<<grid_for(e, e->n), 256, 0, e->stream>>>(e->labels, e->n, e->labels64);
+  CK_LAUNCH("widen_labels_kernel");
+  e->stats.kernel_launches += 1;
+  CK(cudaMemcpyAsync(out, e->labels64, 8 * (size_t)e->n, cudaMemcpyDeviceToHost, e->stream));
+  return KM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* km_version(void) { return "kmeans_b200 0.1.0 (sm_100a)"; }
+
+int km_device_count(int32_t* out) {
+  int c = 0;
+  cudaError_t r = cudaGetDeviceCount(&c);
+  if (r != cudaSuccess) {
+    if (out) *out = 0;
+    cudaGetLastError();
+    return set_err(nullptr, KM_ERR_DEVICE_UNAVAILABLE, "cudaGetDeviceCount: %s", cudaGetErrorString(r));
+  }
+  if (out) *out = c;
+  return KM_OK;
+}
+
+const char* km_last_error(const km_engine* e) { return e ? e->err.c_str() : g_global_err.c_str(); }
+
+int km_create(int32_t device, km_engine** out) {
+  if (!out) return set_err(nullptr, KM_ERR_CONTRACT, "null out pointer");
+  *out = nullptr;
+  int count = 0;
+  cudaError_t r = cudaGetDeviceCount(&count);
+  if (r != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return set_err(nullptr, KM_ERR_DEVICE_UNAVAILABLE, "no CUDA device: %s",
+                   r == cudaSuccess ? "device count is 0" : cudaGetErrorString(r));
+  }
+  if (device < 0 || device >= count)
+    return set_err(nullptr, KM_ERR_DEVICE_UNAVAILABLE, "device %d out of range [0, %d)", device, count);
+  r = cudaSetDevice(device);
+  if (r != cudaSuccess) return set_err(nullptr, KM_ERR_DEVICE_UNAVAILABLE, "cudaSetDevice: %s", cudaGetErrorString(r));
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10)
+    return set_err(nullptr, KM_ERR_DEVICE_UNAVAILABLE, "device %d is sm_%d%d; this build targets sm_100a", device,
+                   prop.major, prop.minor);
+  km_engine* e = new km_engine();
+  e->device = device;
+  e->num_sms = prop.multiProcessorCount;
+  e->smem_optin = prop.sharedMemPerBlockOptin;
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete e;
+    return set_err(nullptr, KM_ERR_DEVICE_LOST, "cudaStreamCreate failed");
+  }
+  e->own_stream = true;
+  if (cudaMalloc((void**)&e->st, sizeof(DevState)) != cudaSuccess ||
+      cudaMallocHost((void**)&e->st_host, sizeof(DevState)) != cudaSuccess ||
+      cudaMalloc((void**)&e->scratch_u, 16) != cudaSuccess || cudaMalloc((void**)&e->scratch_i, 16) != cudaSuccess) {
+    km_destroy(e);
+    return set_err(nullptr, KM_ERR_CAPACITY, "allocation of engine state failed");
+  }
+  std::memset(e->st_host, 0, sizeof(DevState));
+  cudaMemset(e->st, 0, sizeof(DevState));
+  *out = e;
+  return KM_OK;
+}
+
+int km_destroy(km_engine* e) {
+  if (!e) return KM_OK;
+  cudaSetDevice(e->device);
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  drop_points(e);
+  for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
+  dfree(e->st);
+  dfree(e->scratch_u);
+  dfree(e->scratch_i);
+  if (e->st_host) cudaFreeHost(e->st_host);
+  if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
+  delete e;
+  return KM_OK;
+}
+
+int km_set_stream(km_engine* e, void* stream) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  if (stream == nullptr) {
+    if (!e->own_stream) {
+      if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return set_err(e, KM_ERR_DEVICE_LOST, "cudaStreamCreate failed");
+      e->own_stream = true;
+    }
+    return KM_OK;
+  }
+  if (e->own_stream && e->stream) {
+    cudaStreamSynchronize(e->stream);
+    cudaStreamDestroy(e->stream);
+  }
+  e->stream = (cudaStream_t)stream;
+  e->own_stream = false;
+  return KM_OK;
+}
+
+int km_load_points_f32(km_engine* e, const float* x, int64_t n, int32_t m) {
+  int r = validate_points_shape(e, x, n, m);
+  if (r) return r;
+  cudaSetDevice(e->device);
+  drop_points(e);
+  void* d = nullptr;
+  if ((r = dalloc(e, &d, sizeof(float) * (size_t)n * m))) return r;
+  e->x = d;
+  e->x_owned = true;
+  e->n = n;
+  e->m = m;
+  e->point_bytes = 4;
+  CK(cudaMemcpyAsync(d, x, sizeof(float) * (size_t)n * m, cudaMemcpyHostToDevice, e->stream));
+  int flags[2] = {0, 0};
+  if ((r = scan_points(e, d, 4, n * (int64_t)m, flags))) return r;
+  if (flags[0]) { drop_points(e); return set_err(e, KM_ERR_CONTRACT, "coords contains NaN or infinite values"); }
+  return after_points_loaded(e);
+}
+
+int km_load_points_f64(km_engine* e, const double* x, int64_t n, int32_t m) {
+  int r = validate_points_shape(e, x, n, m);
+  if (r) return r;
+  cudaSetDevice(e->device);
+  const int64_t count = n * (int64_t)m;
+  drop_points(e);
+  void* d64 = nullptr;
+  if ((r = dalloc(e, &d64, sizeof(double) * (size_t)count))) return r;
+  CK(cudaMemcpyAsync(d64, x, sizeof(double) * (size_t)count, cudaMemcpyHostToDevice, e->stream));
+  int flags[2] = {0, 0};
+  if ((r = scan_points(e, d64, 8, count, flags))) { cudaFree(d64); return r; }
+  if (flags[0]) { cudaFree(d64); return set_err(e, KM_ERR_CONTRACT, "coords contains NaN or infinite values"); }
+  if (!flags[1]) {  // lossless: keep the fp32 copy only (half the bytes per pass)
+    void* d32 = nullptr;
+    if ((r = dalloc(e, &d32, sizeof(float) * (size_t)count))) { cudaFree(d64); return r; }
+    narrow_f64_kernel<<<grid_for(e, count, 4), 256, 0, e->stream>>>((const double*)d64, count, (float*)d32);
+    cudaError_t c = cudaGetLastError();
+    if (c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
+    cudaFree(d64);
+    if (c != cudaSuccess) { cudaFree(d32); return cuda_fail(e, c, "narrow_f64_kernel"); }
+    e->stats.kernel_launches += 1;
+    e->x = d32;
+    e->point_bytes = 4;
+  } else {
+    e->x = d64;
+    e->point_bytes = 8;
+  }
+  e->x_owned = true;
+  e->n = n;
+  e->m = m;
+  return after_points_loaded(e);
+}
+
+int km_attach_points_device_f32(km_engine* e, const float* dev_x, int64_t n, int32_t m) {
+  int r = validate_points_shape(e, dev_x, n, m);
+  if (r) return r;
+  if (((uintptr_t)dev_x & 15) != 0) return set_err(e, KM_ERR_CONTRACT, "device point buffer must be 16-byte aligned");
+  cudaSetDevice(e->device);
+  drop_points(e);
+  e->x = (void*)dev_x;
+  e->x_owned = false;
+  e->n = n;
+  e->m = m;
+  e->point_bytes = 4;
+  int flags[2] = {0, 0};
+  if ((r = scan_points(e, dev_x, 4, n * (int64_t)m, flags))) return r;
+  if (flags[0]) { drop_points(e); return set_err(e, KM_ERR_CONTRACT, "coords contains NaN or infinite values"); }
+  return after_points_loaded(e);
+}
+
+int km_points_info(km_engine* e, int64_t* n, int32_t* m, int32_t* point_bytes, double* absmax) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (n) *n = e->n;
+  if (m) *m = e->m;
+  if (point_bytes) *point_bytes = e->point_bytes;
+  if (absmax) *absmax = e->absmax;
+  return KM_OK;
+}
+
+static int check_centers(km_engine* e, const double* c, int32_t k) {
+  if (!c) return set_err(e, KM_ERR_CONTRACT, "null centers");
+  if (k < 1) return set_err(e, KM_ERR_CONTRACT, "k must be >= 1, got %d", k);
+  for (int64_t i = 0; i < (int64_t)k * e->m; ++i)
+    if (!std::isfinite(c[i])) return set_err(e, KM_ERR_CONTRACT, "centers contains NaN or infinite values");
+  return KM_OK;
+}
+
+int km_assign(km_engine* e, const double* centers, int32_t k, int64_t* labels_out, int64_t* counts_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if ((r = check_centers(e, centers, k))) return r;
+  if ((r = ensure_k(e, k))) return r;
+  CK(cudaMemcpyAsync(e->cur, centers, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
+  if ((r = reset_state(e, 1, 0.0))) return r;
+  if ((r = launch_prep(e))) return r;
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  if ((r = launch_pass(e, PASS_ASSIGN_ONLY, false))) return r;
+  e->stats.passes += 1;
+  if (labels_out && (r = download_labels(e, labels_out))) return r;
+  if (counts_out)
+    CK(cudaMemcpyAsync(counts_out, e->part + (size_t)k * e->m, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  if ((r = read_state(e))) return r;
+  e->stats.rechecked = (int64_t)e->st_host->rechecked + 0;
+  return KM_OK;
+}
+
+int km_update(km_engine* e, int64_t* labels_inout, int32_t k, double* centers_out, int64_t* counts_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (!labels_inout) return set_err(e, KM_ERR_CONTRACT, "null labels");
+  if (k < 1) return set_err(e, KM_ERR_CONTRACT, "k must be >= 1, got %d", k);
+  std::vector<int32_t> lab((size_t)e->n);
+  for (int64_t i = 0; i < e->n; ++i) {
+    const int64_t v = labels_inout[i];
+    if (v < 0 || v >= k) return set_err(e, KM_ERR_CONTRACT, "labels must lie in [0, %d)", k);
+    lab[i] = (int32_t)v;
+  }
+  if ((r = ensure_k(e, k))) return r;
+  CK(cudaMemcpyAsync(e->labels, lab.data(), 4 * (size_t)e->n, cudaMemcpyHostToDevice, e->stream));
+  if ((r = reset_state(e, 1, 0.0))) return r;
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  if ((r = launch_pass(e, PASS_SUMS_ONLY, false))) return r;
+  if ((r = launch_finish(e, 1))) return r;
+  if ((r = read_state(e))) return r;
+  if (e->st_host->bad_label) return set_err(e, KM_ERR_VALIDATION, "label out of range [0, %d) on device", k);
+  const bool repaired = e->st_host->n_empty > 0;
+  if (repaired && (r = repair_local(e))) return r;
+  if (centers_out) CK(cudaMemcpyAsync(centers_out, e->cur, 8 * (size_t)k * e->m, cudaMemcpyDeviceToHost, e->stream));
+  if (counts_out) CK(cudaMemcpyAsync(counts_out, e->model_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
+  if (repaired) {
+    CK(cudaMemcpyAsync(lab.data(), e->labels, 4 * (size_t)e->n, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    for (int64_t i = 0; i < e->n; ++i) labels_inout[i] = lab[i];
+  }
+  CK(cudaStreamSynchronize(e->stream));
+  return KM_OK;
+}
+
+int km_converged(km_engine* e, const double* prev, const double* next, int32_t k, int32_t m, double tol,
+                 int32_t* out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!prev || !next || !out) return set_err(e, KM_ERR_CONTRACT, "null argument");
+  if (k < 1 || m < 1) return set_err(e, KM_ERR_CONTRACT, "bad shape (%d, %d)", k, m);
+  if (!(tol >= 0.0)) return set_err(e, KM_ERR_CONTRACT, "tol must be >= 0, got %g", tol);
+  cudaSetDevice(e->device);
+  double* buf = nullptr;
+  int r;
+  if ((r = dalloc(e, &buf, 8 * 2 * (size_t)k * m))) return r;
+  int32_t* flag = e->scratch_i;
+  cudaMemcpyAsync(buf, prev, 8 * (size_t)k * m, cudaMemcpyHostToDevice, e->stream);
+  cudaMemcpyAsync(buf + (size_t)k * m, next, 8 * (size_t)k * m, cudaMemcpyHostToDevice, e->stream);
+  converged_kernel<<<1, finish_threads(k, 1), 0, e->stream>>>(buf, buf + (size_t)k * m, k, m, tol, flag);
+  cudaError_t c = cudaGetLastError();
+  int32_t h = 0;
+  if (c == cudaSuccess) c = cudaMemcpyAsync(&h, flag, 4, cudaMemcpyDeviceToHost, e->stream);
+  if (c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
+  cudaFree(buf);
+  if (c != cudaSuccess) return cuda_fail(e, c, "km_converged");
+  *out = h;
+  return KM_OK;
+}
+
+int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, double tol, double* centers_out,
+             int64_t* counts_out, int64_t* labels_out, int32_t* iterations_out, int32_t* converged_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (max_iters < 1) return set_err(e, KM_ERR_CONTRACT, "max_iters must be >= 1, got %d", max_iters);
+  if (!(tol >= 0.0)) return set_err(e, KM_ERR_CONTRACT, "tol must be >= 0, got %g", tol);
+  if (k > e->n) return set_err(e, KM_ERR_CONTRACT, "k=%d exceeds sample count n=%lld", k, (long long)e->n);
+  if ((r = check_centers(e, c0, k))) return r;
+  if ((r = ensure_k(e, k))) return r;
+  CK(cudaMemcpyAsync(e->cur, c0, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
+  if ((r = reset_state(e, max_iters, tol))) return r;
+  if ((r = launch_prep(e))) return r;
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  int batch = 1;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
+  auto timed_pass = [&](void) -> int {
+    if (!e->profiling) return launch_pass(e, PASS_ASSIGN_SUMS, true);
+    const size_t need = 2 * (timed.size() + 1);
+    while (e->ev.size() < need) {
+      cudaEvent_t ev;
+      CK(cudaEventCreate(&ev));
+      e->ev.push_back(ev);
+    }
+    cudaEvent_t a = e->ev[need - 2], b = e->ev[need - 1];
+    CK(cudaEventRecord(a, e->stream));
+    int rr = launch_pass(e, PASS_ASSIGN_SUMS, true);
+    if (rr) return rr;
+    CK(cudaEventRecord(b, e->stream));
+    timed.push_back({a, b});
+    return KM_OK;
+  };
+  // account the passes of a batch that actually ran (gated passes after
+  // done / need_host exit immediately and are not counted)
+  auto account = [&](int n_ran) -> int {
+    for (int i = 0; i < (int)timed.size() && i < n_ran; ++i) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, timed[i].first, timed[i].second));
+      e->stats.pass_ms_total += ms;
+      e->stats.pass_timed += 1;
+    }
+    timed.clear();
+    return KM_OK;
+  };
+  // L0 = A(C0) (engine.py:328), fused with the sums U(L0) needs.
+  if ((r = timed_pass())) return r;
+  int first = 1;
+  int t_before = 0;
+  for (;;) {
+    for (int b = 0; b < batch; ++b) {
+      if ((r = launch_finish(e, 0))) return r;
+      if ((r = timed_pass())) return r;
+    }
+    if ((r = read_state(e))) return r;
+    const DevState s = *e->st_host;
+    const int ran_updates = s.t - t_before;
+    const int stopped = (s.done && s.converged) || s.need_host ? 1 : 0;
+    if ((r = account(first + std::max(0, ran_updates - stopped)))) return r;
+    first = 0;
+    t_before = s.t;
+    if (s.done) break;
+    if (s.need_host) {
+      if ((r = repair_local(e))) return r;
+      if ((r = launch_check(e))) return r;
+      if ((r = timed_pass())) return r;
+      // the check may have finished the loop (converged): then the pass was gated
+      if ((r = read_state(e))) return r;
+      if ((r = account(e->st_host->done ? 0 : 1))) return r;
+      if (e->st_host->done) break;
+      batch = 1;
+      continue;
+    }
+    batch = std::min(batch * 2, 16);
+  }
+  const DevState s = *e->st_host;
+  e->stats.passes += 1 + s.t - (s.converged ? 1 : 0);
+  e->stats.rechecked = (int64_t)s.rechecked;
+  if (centers_out) CK(cudaMemcpyAsync(centers_out, e->cur, 8 * (size_t)k * e->m, cudaMemcpyDeviceToHost, e->stream));
+  if (counts_out) {
+    const void* src = s.converged ? (const void*)e->model_counts : (const void*)(e->part + (size_t)k * e->m);
+    CK(cudaMemcpyAsync(counts_out, src, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
+  }
+  if (labels_out && (r = download_labels(e, labels_out))) return r;
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  if (iterations_out) *iterations_out = s.t;
+  if (converged_out) *converged_out = s.converged;
+  return KM_OK;
+}
+
+int km_wcss(km_engine* e, const double* centers, int32_t k, const int64_t* labels, double* out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (!out || !labels) return set_err(e, KM_ERR_CONTRACT, "null argument");
+  if ((r = check_centers(e, centers, k))) return r;
+  std::vector<int32_t> lab((size_t)e->n);
+  for (int64_t i = 0; i < e->n; ++i) {
+    if (labels[i] < 0 || labels[i] >= k) return set_err(e, KM_ERR_CONTRACT, "labels must lie in [0, %d)", k);
+    lab[i] = (int32_t)labels[i];
+  }
+  if ((r = ensure_k(e, k))) return r;
+  CK(cudaMemcpyAsync(e->scratch_d, centers, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
+  CK(cudaMemcpyAsync(e->labels, lab.data(), 4 * (size_t)e->n, cudaMemcpyHostToDevice, e->stream));
+  // bound every term: d2 ≤ m·(2·max(|x|,|c|))²
+  double cm = e->absmax;
+  for (int64_t i = 0; i < (int64_t)k * e->m; ++i) cm = std::max(cm, std::fabs(centers[i]));
+  const double term = (double)e->m * 4.0 * cm * cm;
+  const int F2 = compute_frac_bits(std::max(term, 1e-300), e->n);
+  unsigned long long zero = 0;
+  CK(cudaMemcpyAsync(e->scratch_u, &zero, 8, cudaMemcpyHostToDevice, e->stream));
+  const int g = grid_for(e, e->n);
+  if (e->point_bytes == 4)
+    wcss_kernel<float><<<g, 256, 0, e->stream>>>((const float*)e->x, e->n, e->m, e->scratch_d, e->labels,
+                                                 std::ldexp(1.0, F2), e->scratch_u);
+  else
+    wcss_kernel<double><<<g, 256, 0, e->stream>>>((const double*)e->x, e->n, e->m, e->scratch_d, e->labels,
+                                                  std::ldexp(1.0, F2), e->scratch_u);
+  CK_LAUNCH("wcss_kernel");
+  unsigned long long v = 0;
+  CK(cudaMemcpyAsync(&v, e->scratch_u, 8, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  *out = std::ldexp((double)(long long)v, -F2);
+  return KM_OK;
+}
+
+int km_center_distances(km_engine* e, const double* centers, int32_t k, double* out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (!out) return set_err(e, KM_ERR_CONTRACT, "null argument");
+  if ((r = check_centers(e, centers, k))) return r;
+  double* cbuf = nullptr;
+  double* obuf = nullptr;
+  if ((r = dalloc(e, &cbuf, 8 * (size_t)k * e->m))) return r;
+  if ((r = dalloc(e, &obuf, 8 * (size_t)e->n * k))) { cudaFree(cbuf); return r; }
+  cudaMemcpyAsync(cbuf, centers, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream);
+  const int g = grid_for(e, e->n * (int64_t)k);
+  if (e->point_bytes == 4)
+    center_distances_kernel<float><<<g, 256, 0, e->stream>>>((const float*)e->x, e->n, e->m, cbuf, k, obuf);
+  else
+    center_distances_kernel<double><<<g, 256, 0, e->stream>>>((const double*)e->x, e->n, e->m, cbuf, k, obuf);
+  cudaError_t c = cudaGetLastError();
+  if (c == cudaSuccess) c = cudaMemcpyAsync(out, obuf, 8 * (size_t)e->n * k, cudaMemcpyDeviceToHost, e->stream);
+  if (c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
+  cudaFree(cbuf);
+  cudaFree(obuf);
+  if (c != cudaSuccess) return cuda_fail(e, c, "km_center_distances");
+  return KM_OK;
+}
+
+// ---- step API (row-sharded multi-GPU) --------------------------------------
+int km_frac_bits_for(double absmax, int64_t n_total, int32_t* out) {
+  if (!out) return set_err(nullptr, KM_ERR_CONTRACT, "null out");
+  *out = compute_frac_bits(absmax, n_total);
+  return KM_OK;
+}
+
+int km_set_frac_bits(km_engine* e, int32_t frac_bits) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  e->frac_bits = frac_bits;
+  e->frac_user = true;
+  e->stats.frac_bits = frac_bits;
+  return KM_OK;
+}
+
+int km_step_begin(km_engine* e, const double* c0, int32_t k) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if ((r = check_centers(e, c0, k))) return r;
+  if ((r = ensure_k(e, k))) return r;
+  CK(cudaMemcpyAsync(e->cur, c0, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
+  if ((r = reset_state(e, INT32_MAX, 0.0))) return r;
+  if ((r = launch_prep(e))) return r;
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  return KM_OK;
+}
+
+int km_step_partials(km_engine* e, void** dev_ptr, int64_t* n_int64) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->part) return set_err(e, KM_ERR_CONTRACT, "call km_step_begin first");
+  if (dev_ptr) *dev_ptr = e->part;
+  if (n_int64) *n_int64 = (int64_t)e->k * e->m + e->k;
+  return KM_OK;
+}
+
+int km_step_pass(km_engine* e) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->part) return set_err(e, KM_ERR_CONTRACT, "call km_step_begin first");
+  cudaSetDevice(e->device);
+  int r = launch_pass(e, PASS_ASSIGN_SUMS, false);
+  if (r) return r;
+  e->stats.passes += 1;
+  CK(cudaStreamSynchronize(e->stream));
+  return KM_OK;
+}
+
+int km_step_finish(km_engine* e, double tol, int32_t* status_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->part) return set_err(e, KM_ERR_CONTRACT, "call km_step_begin first");
+  cudaSetDevice(e->device);
+  int r;
+  // keep the loop ungated: clear done/need_host, set tol
+  CK(cudaMemcpyAsync(e->st_host, e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  e->st_host->done = 0;
+  e->st_host->need_host = 0;
+  e->st_host->exhausted = 0;
+  e->st_host->converged = 0;
+  e->st_host->tol = tol;
+  e->st_host->max_iters = INT32_MAX;
+  CK(cudaMemcpyAsync(e->st, e->st_host, sizeof(DevState), cudaMemcpyHostToDevice, e->stream));
+  if ((r = launch_finish(e, 0))) return r;
+  if ((r = read_state(e))) return r;
+  if (status_out) {
+    status_out[0] = e->st_host->n_empty;
+    status_out[1] = e->st_host->converged;
+  }
+  return KM_OK;
+}
+
+int km_step_repair_prepare(km_engine* e) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  return self_d2(e);
+}
+
+int km_step_repair_candidate(km_engine* e, double* d2_out, int64_t* row_out, double* coords_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->d2) return set_err(e, KM_ERR_CONTRACT, "call km_step_repair_prepare first");
+  cudaSetDevice(e->device);
+  argmax_partial_kernel<<<e->n_partials, 256, 0, e->stream>>>(e->d2, e->n, e->partials);
+  CK_LAUNCH("argmax_partial_kernel");
+  argmax_final_kernel<<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, e->winner);
+  CK_LAUNCH("argmax_final_kernel");
+  ArgMax h{};
+  CK(cudaMemcpyAsync(&h, e->winner, sizeof h, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  if (d2_out) *d2_out = h.v;
+  if (row_out) *row_out = h.i;
+  if (coords_out && h.i >= 0 && h.i < e->n) {
+    if (e->point_bytes == 4) {
+      std::vector<float> row(e->m);
+      CK(cudaMemcpy(row.data(), (const float*)e->x + h.i * e->m, 4 * (size_t)e->m, cudaMemcpyDeviceToHost));
+      for (int f = 0; f < e->m; ++f) coords_out[f] = row[f];
+    } else {
+      CK(cudaMemcpy(coords_out, (const double*)e->x + h.i * e->m, 8 * (size_t)e->m, cudaMemcpyDeviceToHost));
+    }
+  }
+  return KM_OK;
+}
+
+int km_step_label_of(km_engine* e, int64_t local_row, int32_t* label_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (local_row < 0 || local_row >= e->n) return set_err(e, KM_ERR_CONTRACT, "row out of range");
+  cudaSetDevice(e->device);
+  CK(cudaMemcpyAsync(label_out, e->labels + local_row, 4, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  return KM_OK;
+}
+
+int km_step_repair_apply(km_engine* e, int32_t empty_cluster, int32_t owner_is_me, int64_t local_row,
+                         const double* coords, int32_t donor) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!coords) return set_err(e, KM_ERR_CONTRACT, "null coords");
+  if (empty_cluster < 0 || empty_cluster >= e->k || donor < 0 || donor >= e->k)
+    return set_err(e, KM_ERR_CONTRACT, "cluster index out of range");
+  cudaSetDevice(e->device);
+  double* dc = e->scratch_d;
+  CK(cudaMemcpyAsync(dc, coords, 8 * (size_t)e->m, cudaMemcpyHostToDevice, e->stream));
+  repair_apply_global_kernel<<<1, 32, 0, e->stream>>>(empty_cluster, owner_is_me, local_row, dc, donor, e->m,
+                                                             e->labels, e->d2, e->model_counts, e->cur);
+  CK_LAUNCH("repair_apply_global_kernel");
+  CK(cudaStreamSynchronize(e->stream));
+  e->stats.repairs += 1;
+  return KM_OK;
+}
+
+int km_step_empty_list(km_engine* e, int32_t* empties_out, int32_t* n_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  std::vector<int32_t> v;
+  int r = empty_list(e, v);
+  if (r) return r;
+  if (n_out) *n_out = (int32_t)v.size();
+  if (empties_out) std::copy(v.begin(), v.end(), empties_out);
+  return KM_OK;
+}
+
+int km_step_check(km_engine* e, double tol, int32_t* converged_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  CK(cudaMemcpyAsync(e->st_host, e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  e->st_host->tol = tol;
+  e->st_host->max_iters = INT32_MAX;
+  CK(cudaMemcpyAsync(e->st, e->st_host, sizeof(DevState), cudaMemcpyHostToDevice, e->stream));
+  if ((r = launch_check(e))) return r;
+  if ((r = read_state(e))) return r;
+  if (converged_out) *converged_out = e->st_host->converged;
+  return KM_OK;
+}
+
+int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, int64_t* labels_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (centers_out) CK(cudaMemcpyAsync(centers_out, e->cur, 8 * (size_t)e->k * e->m, cudaMemcpyDeviceToHost, e->stream));
+  if (counts_out) CK(cudaMemcpyAsync(counts_out, e->model_counts, 8 * (size_t)e->k, cudaMemcpyDeviceToHost, e->stream));
+  if (labels_out && (r = download_labels(e, labels_out))) return r;
+  CK(cudaStreamSynchronize(e->stream));
+  return KM_OK;
+}
+
+int km_reset_stats(km_engine* e) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  const int32_t fb = e->stats.frac_bits, pb = e->stats.point_bytes;
+  e->stats = km_stats{};
+  e->stats.frac_bits = fb;
+  e->stats.point_bytes = pb;
+  return KM_OK;
+}
+
+int km_set_profiling(km_engine* e, int32_t enable) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  e->profiling = enable != 0;
+  return KM_OK;
+}
+
+int km_get_stats(km_engine* e, km_stats* out) {
+  if (!e || !out) return set_err(e, KM_ERR_CONTRACT, "null argument");
+  *out = e->stats;
+  return KM_OK;
+}
+
+}  // extern "C"

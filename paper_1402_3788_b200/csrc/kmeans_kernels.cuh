@@ -1,0 +1,583 @@
+// kmeans_kernels.cuh — device code of the B200 Lloyd engine.
+//
+// One Lloyd iteration = ONE fused pass over the resident point matrix
+// (assign + per-cluster fixed-point sums) followed by a one-CTA finish kernel
+// (divide, empty-cluster count, convergence flag, fp32 filter prep).
+//
+// Arithmetic contract (what makes labels bit-identical to the reference):
+//  * Labels are decided by a certified fp32 filter.  Score
+//        S~_c = fl(‖c~‖² + Σ_f x~_f·(−2c~_f))      (M FMAs, features ascending)
+//    differs from the exact ‖x−c‖² − ‖x‖² by at most
+//        E = coef·(‖x‖ + max_c‖c‖)²,  coef = (M+8)·2⁻²⁴·1.25
+//    (FMA-chain γ_M bound + rounding of x, c, ‖c‖² to fp32 + the fp64
+//    rounding of the reference's own distance).  When the
+//    runner-up score exceeds best + 2E the fp32 argmin IS the reference
+//    argmin.  Otherwise every centre with S~_c ≤ best + 2E is re-decided with
+//    the reference's exact fp64 recurrence (_kernels.py:31-44: d = x−c,
+//    acc += d*d, no FMA, ascending c, strict '<' keeps the lowest index).
+//  * Cluster sums are int64 fixed point with 2^F scaling (F chosen from
+//    max|x| and n so no sum can overflow): integer adds are associative, so the
+//    sums — and the centres — are bit-identical for any grid size and any
+//    number of GPUs (the reference gets the same property from canonical
+//    blocks, model.py:18-24; we get it from exact integer arithmetic).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace km {
+
+constexpr int kTileRows = 256;   // rows per CTA tile == threads per CTA
+constexpr int kThreads = 256;
+
+// Device-side loop state (lives in device memory, mirrored to pinned host).
+struct DevState {
+  int32_t t;          // updates performed (reference `iterations`)
+  int32_t done;       // loop finished
+  int32_t converged;  // finished by convergence
+  int32_t exhausted;  // t == max_iters without convergence: one more assign pass, then done
+  int32_t need_host;  // empty clusters: host must run the repair before the check
+  int32_t n_empty;
+  int32_t max_iters;
+  int32_t bad_label;  // first invalid label seen by a sums-only pass (+1), 0 = none
+  unsigned long long rechecked;
+  double tol;
+};
+
+struct PassArgs {
+  const void* x;          // n × m row-major, T = float or double
+  int64_t n;
+  int32_t m, k;
+  const float* w;         // k × MPAD: −2·fl32(c)  (zero padded)
+  const float* cn;        // k: fl32(‖fl32(c)‖²)
+  const float* cmax;      // [0]: max_c ‖fl32(c)‖ rounded up
+  const double* c64;      // k × m reference-precision centres (for the exact recheck)
+  int32_t* labels;        // n
+  unsigned long long* part;  // k·m sums (fixed point, two's complement) then k counts
+  float scale_f;          // 2^F as float (valid when !use_dscale)
+  double scale_d;         // 2^F
+  int32_t use_dscale;
+  int32_t mpad;           // row pitch of w
+  float err_coef;         // (M+8)·2^-24·1.25
+  float err_floor;        // absolute floor for subnormal effects
+  float nx_inflate;       // 1 + (M+2)·2^-24
+  int32_t exact_only;     // filter disabled (extreme magnitudes): fp64 for every centre
+  DevState* st;           // loop state (statistics; gating when `gate`)
+  int32_t gate;           // early-exit when the loop is done / waiting for the host
+};
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T v) { return (float)v; }
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T v) { return (double)v; }
+
+// Reference recurrence for one squared distance (_kernels.py:33-41): no FMA.
+template <typename T>
+__device__ __forceinline__ double exact_d2(const T* xrow, const double* __restrict__ c, int m) {
+  double acc = 0.0;
+  for (int f = 0; f < m; ++f) {
+    double d = __dsub_rn(to_f64(xrow[f]), c[f]);
+    acc = __dadd_rn(acc, __dmul_rn(d, d));
+  }
+  return acc;
+}
+
+template <typename T>
+__device__ __forceinline__ long long to_fixed(T v, float sf, double sd, int use_d);
+
+template <>
+__device__ __forceinline__ long long to_fixed<float>(float v, float sf, double sd, int use_d) {
+  return use_d ? __double2ll_rn(__dmul_rn((double)v, sd)) : __float2ll_rn(__fmul_rn(v, sf));
+}
+template <>
+__device__ __forceinline__ long long to_fixed<double>(double v, float, double sd, int) {
+  return __double2ll_rn(__dmul_rn(v, sd));
+}
+
+// fp32 filter score of centre c for a point held in registers.
+template <int MP>
+__device__ __forceinline__ float score_reg(const float (&xr)[MP], const float* __restrict__ wc, float cn) {
+  float a = cn;
+#pragma unroll
+  for (int f = 0; f < MP; f += 4) {
+    const float4 w4 = *reinterpret_cast<const float4*>(wc + f);
+    a = __fmaf_rn(xr[f + 0], w4.x, a);
+    a = __fmaf_rn(xr[f + 1], w4.y, a);
+    a = __fmaf_rn(xr[f + 2], w4.z, a);
+    a = __fmaf_rn(xr[f + 3], w4.w, a);
+  }
+  return a;
+}
+
+// Generic-M filter score, x read from the shared-memory tile.
+template <typename T>
+__device__ __forceinline__ float score_smem(const T* xrow, int m, const float* __restrict__ wc, float cn) {
+  float a = cn;
+  for (int f = 0; f < m; ++f) a = __fmaf_rn(to_f32(xrow[f]), wc[f], a);
+  return a;
+}
+
+// Cooperative copy of `bytes` (multiple of 4) from global to shared, 16 B vectors
+// where the source is 16 B aligned (it is: cudaMalloc base + tile offsets that
+// are multiples of 1 KiB).
+__device__ __forceinline__ void tile_copy(void* dst, const void* src, int64_t bytes) {
+  const int64_t nv = bytes >> 4;
+  const float4* s4 = reinterpret_cast<const float4*>(src);
+  float4* d4 = reinterpret_cast<float4*>(dst);
+  for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d4[i] = __ldg(s4 + i);
+  const int64_t tail = (bytes - (nv << 4)) >> 2;
+  const float* s1 = reinterpret_cast<const float*>(src) + (nv << 2);
+  float* d1 = reinterpret_cast<float*>(dst) + (nv << 2);
+  for (int64_t i = threadIdx.x; i < tail; i += blockDim.x) d1[i] = __ldg(s1 + i);
+}
+
+// ---------------------------------------------------------------------------
+// Fused pass: labels + per-cluster fixed-point sums + counts.
+//   DO_ASSIGN: compute labels (else read them and validate, update_step path)
+//   DO_SUMS:   accumulate coordinate sums (counts are always accumulated)
+//   MP:        padded feature count held in registers (0 = generic, from smem)
+//   SMEM_ACC:  privatised per-CTA accumulators in shared memory
+// ---------------------------------------------------------------------------
+template <typename T, int MP, bool DO_ASSIGN, bool DO_SUMS, bool SMEM_ACC>
+__global__ void __launch_bounds__(kThreads) lloyd_pass_kernel(PassArgs a) {
+  if (a.gate && (a.st->done || a.st->need_host)) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int m = a.m, k = a.k, tid = threadIdx.x;
+  const int mpad = a.mpad;
+  // layout: [acc k*m u64][cnt k u64][w k*mpad f32][cn k f32][tile 256*m T]
+  unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* s_cnt = s_acc + (SMEM_ACC ? (size_t)k * m : 0);
+  float* s_w = reinterpret_cast<float*>(s_cnt + (SMEM_ACC ? k : 0));
+  float* s_cn = s_w + (DO_ASSIGN ? (size_t)k * mpad : 0);
+  size_t off = reinterpret_cast<unsigned char*>(s_cn + (DO_ASSIGN ? k : 0)) - smem;
+  off = (off + 15) & ~size_t(15);
+  T* s_tile = reinterpret_cast<T*>(smem + off);
+
+  if (SMEM_ACC) {
+    for (int i = tid; i < k * m + k; i += kThreads) s_acc[i] = 0ull;
+  }
+  if (DO_ASSIGN) {
+    for (int i = tid; i < k * mpad; i += kThreads) s_w[i] = a.w[i];
+    for (int i = tid; i < k; i += kThreads) s_cn[i] = a.cn[i];
+  }
+  unsigned long long* g_acc = a.part;
+  unsigned long long* g_cnt = a.part + (size_t)k * m;
+  unsigned long long* acc = SMEM_ACC ? s_acc : g_acc;
+  unsigned long long* cnt = SMEM_ACC ? s_cnt : g_cnt;
+
+  const float cmax = DO_ASSIGN ? a.cmax[0] : 0.f;
+  const T* __restrict__ X = reinterpret_cast<const T*>(a.x);
+  const int64_t ntiles = (a.n + kTileRows - 1) / kTileRows;
+  unsigned int my_rechecks = 0;
+  int bad = 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t row0 = tile * kTileRows;
+    const int64_t rem = a.n - row0;
+    const int rows = rem < kTileRows ? (int)rem : kTileRows;
+    __syncthreads();  // previous tile fully consumed (and smem init done)
+    tile_copy(s_tile, X + row0 * m, (int64_t)rows * m * (int64_t)sizeof(T));
+    __syncthreads();
+    if (tid < rows) {
+      const T* xrow = s_tile + (size_t)tid * m;
+      int lab;
+      if (DO_ASSIGN) {
+        float best = __int_as_float(0x7f800000), min2 = best;
+        int bi = 0;
+        float nx2 = 0.f;
+        if constexpr (MP > 0) {
+          float xr[MP];
+#pragma unroll
+          for (int f = 0; f < MP; ++f) xr[f] = (f < m) ? to_f32(xrow[f]) : 0.f;
+#pragma unroll
+          for (int f = 0; f < MP; ++f) nx2 = __fmaf_rn(xr[f], xr[f], nx2);
+          for (int c = 0; c < k; ++c) {
+            const float s = score_reg<MP>(xr, s_w + (size_t)c * mpad, s_cn[c]);
+            const bool lt = s < best;
+            min2 = lt ? best : fminf(min2, s);
+            bi = lt ? c : bi;
+            best = lt ? s : best;
+          }
+          const float t = __fmaf_rn(sqrtf(nx2), a.nx_inflate, cmax);
+          const float E = __fmaf_rn(a.err_coef * t, t, a.err_floor);
+          const float thr = best + 2.f * E;
+          if (a.exact_only || !(min2 > thr)) {
+            ++my_rechecks;
+            double bd = 0.0;
+            int bl = -1;
+            for (int c = 0; c < k; ++c) {
+              bool cand = a.exact_only != 0;
+              if (!cand) cand = score_reg<MP>(xr, s_w + (size_t)c * mpad, s_cn[c]) <= thr;
+              if (cand) {
+                const double d = exact_d2<T>(xrow, a.c64 + (size_t)c * m, m);
+                if (bl < 0 || d < bd) { bd = d; bl = c; }
+              }
+            }
+            bi = bl;
+          }
+        } else {
+          for (int f = 0; f < m; ++f) { const float v = to_f32(xrow[f]); nx2 = __fmaf_rn(v, v, nx2); }
+          for (int c = 0; c < k; ++c) {
+            const float s = score_smem<T>(xrow, m, s_w + (size_t)c * mpad, s_cn[c]);
+            const bool lt = s < best;
+            min2 = lt ? best : fminf(min2, s);
+            bi = lt ? c : bi;
+            best = lt ? s : best;
+          }
+          const float t = __fmaf_rn(sqrtf(nx2), a.nx_inflate, cmax);
+          const float E = __fmaf_rn(a.err_coef * t, t, a.err_floor);
+          const float thr = best + 2.f * E;
+          if (a.exact_only || !(min2 > thr)) {
+            ++my_rechecks;
+            double bd = 0.0;
+            int bl = -1;
+            for (int c = 0; c < k; ++c) {
+              bool cand = a.exact_only != 0;
+              if (!cand) cand = score_smem<T>(xrow, m, s_w + (size_t)c * mpad, s_cn[c]) <= thr;
+              if (cand) {
+                const double d = exact_d2<T>(xrow, a.c64 + (size_t)c * m, m);
+                if (bl < 0 || d < bd) { bd = d; bl = c; }
+              }
+            }
+            bi = bl;
+          }
+        }
+        lab = bi;
+        a.labels[row0 + tid] = lab;
+      } else {
+        lab = a.labels[row0 + tid];
+        if (lab < 0 || lab >= k) { bad = 1; lab = -1; }
+      }
+      if (lab >= 0) {
+        atomicAdd(cnt + lab, 1ull);
+        if (DO_SUMS) {
+          unsigned long long* dst = acc + (size_t)lab * m;
+          for (int f = 0; f < m; ++f)
+            atomicAdd(dst + f, (unsigned long long)to_fixed<T>(xrow[f], a.scale_f, a.scale_d, a.use_dscale));
+        }
+      }
+    }
+  }
+  // statistics / validation
+  if (DO_ASSIGN) {
+    unsigned int wsum = my_rechecks;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+    if ((tid & 31) == 0 && wsum) atomicAdd(&a.st->rechecked, (unsigned long long)wsum);
+  }
+  if (!DO_ASSIGN && bad) atomicExch(&a.st->bad_label, 1);
+  if (SMEM_ACC) {
+    __syncthreads();
+    for (int i = tid; i < k * m; i += kThreads)
+      if (s_acc[i]) atomicAdd(g_acc + i, s_acc[i]);
+    for (int i = tid; i < k; i += kThreads)
+      if (s_cnt[i]) atomicAdd(g_cnt + i, s_cnt[i]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Finish (one CTA): C_t = S/N (engine._finish_update, engine.py:249-263),
+// empty-cluster count, then — if no cluster is empty — the congruence test
+// (engine.converged, engine.py:297-310) and the fp32 filter prep.
+// ---------------------------------------------------------------------------
+struct FinishArgs {
+  unsigned long long* part;  // k·m sums + k counts (zeroed after use unless the loop ends)
+  double* cur;               // k × m current centres (in: C_{t-1}; out: C_t)
+  double* prev;              // k × m (out: C_{t-1})
+  long long* model_counts;   // k (out)
+  float* w;                  // k × mpad (out: −2·fl32(C_t))
+  float* cn;                 // k
+  float* cmax;               // [0]
+  int32_t k, m, mpad;
+  double inv_scale;          // 2^-F
+  DevState* st;
+  int32_t mode;              // 0 = loop iteration, 1 = standalone update (no state machine)
+};
+
+__device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, float* w, float* cn, float* cmax,
+                                                  int k, int m, int mpad, float* s_red) {
+  // w = −2·fl32(c) (exact scaling), cn = fl32(Σ fl32(c)²), cmax = max √(Σ fl32(c)²) rounded up.
+  for (int i = threadIdx.x; i < k * mpad; i += blockDim.x) {
+    const int cc = i / mpad, f = i - cc * mpad;
+    w[i] = (f < m) ? -2.0f * __double2float_rn(c[(size_t)cc * m + f]) : 0.0f;
+  }
+  float local_max = 0.f;
+  for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
+    double s = 0.0;
+    for (int f = 0; f < m; ++f) {
+      const double v = (double)__double2float_rn(c[(size_t)cc * m + f]);
+      s = __fma_rn(v, v, s);
+    }
+    cn[cc] = __double2float_rn(s);
+    const float r = __double2float_ru(sqrt(s) * (1.0 + 1e-12));
+    local_max = fmaxf(local_max, r);
+  }
+  // block max
+  for (int o = 16; o > 0; o >>= 1) local_max = fmaxf(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local_max;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mx = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_red[i]);
+    cmax[0] = mx;
+  }
+  __syncthreads();
+}
+
+// worst = max_c sqrt(Σ_f (prev−next)²) ≤ tol, fp64, no FMA (engine.py:306-310, _kernels.py:173-180)
+__device__ __forceinline__ int block_converged(const double* __restrict__ prev, const double* __restrict__ next,
+                                               int k, int m, double tol, double* s_redd) {
+  double worst = 0.0;
+  for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
+    double acc = 0.0;
+    for (int f = 0; f < m; ++f) {
+      const double d = __dsub_rn(prev[(size_t)cc * m + f], next[(size_t)cc * m + f]);
+      acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    worst = fmax(worst, sqrt(acc));
+  }
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  if ((threadIdx.x & 31) == 0) s_redd[threadIdx.x >> 5] = worst;
+  __syncthreads();
+  double w = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) w = fmax(w, s_redd[i]);
+  __syncthreads();
+  return w <= tol ? 1 : 0;
+}
+
+__device__ __forceinline__ void loop_check(FinishArgs& a, double* s_redd, float* s_red) {
+  DevState* st = a.st;
+  const int conv = block_converged(a.prev, a.cur, a.k, a.m, st->tol, s_redd);
+  block_prep_filter(a.cur, a.w, a.cn, a.cmax, a.k, a.m, a.mpad, s_red);
+  if (threadIdx.x == 0) {
+    st->need_host = 0;
+    if (conv) {
+      st->converged = 1;
+      st->done = 1;
+    } else if (st->t >= st->max_iters) {
+      st->exhausted = 1;  // reference: assignment = assign_fn(model) once more, then return
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a) {
+  __shared__ float s_red[32];
+  __shared__ double s_redd[32];
+  __shared__ int s_empty[32];
+  DevState* st = a.st;
+  if (a.mode == 0) {
+    if (st->done || st->need_host) return;
+    if (st->exhausted) {  // the final assign pass has run: L_T and bincount(L_T) are in place
+      if (threadIdx.x == 0) st->done = 1;
+      return;
+    }
+  }
+  const int k = a.k, m = a.m;
+  unsigned long long* sums = a.part;
+  unsigned long long* cnts = a.part + (size_t)k * m;
+  // prev ← cur ; cur ← S/N
+  for (int i = threadIdx.x; i < k * m; i += blockDim.x) {
+    const int cc = i / m;
+    const long long nc = (long long)cnts[cc];
+    a.prev[i] = a.cur[i];
+    if (nc > 0) {
+      const double s = __dmul_rn((double)(long long)sums[i], a.inv_scale);
+      a.cur[i] = __ddiv_rn(s, (double)nc);
+    } else {
+      a.cur[i] = 0.0;  // placeholder; every empty cluster is re-seeded by the repair
+    }
+  }
+  int empties = 0;
+  for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
+    const long long nc = (long long)cnts[cc];
+    a.model_counts[cc] = nc;
+    empties += (nc == 0);
+  }
+  for (int o = 16; o > 0; o >>= 1) empties += __shfl_xor_sync(0xffffffffu, empties, o);
+  if ((threadIdx.x & 31) == 0) s_empty[threadIdx.x >> 5] = empties;
+  __syncthreads();
+  int total_empty = 0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) total_empty += s_empty[i];
+  // consumed: zero the accumulators for the next pass
+  for (int i = threadIdx.x; i < k * m + k; i += blockDim.x) a.part[i] = 0ull;
+  if (a.mode == 1) {
+    if (threadIdx.x == 0) st->n_empty = total_empty;
+    return;
+  }
+  if (threadIdx.x == 0) {
+    st->t += 1;
+    st->n_empty = total_empty;
+  }
+  __syncthreads();
+  if (total_empty > 0) {
+    if (threadIdx.x == 0) st->need_host = 1;
+    return;
+  }
+  loop_check(a, s_redd, s_red);
+}
+
+// After a host-driven repair: congruence test + prep (no division).
+__global__ void __launch_bounds__(512) lloyd_check_kernel(FinishArgs a) {
+  __shared__ float s_red[32];
+  __shared__ double s_redd[32];
+  loop_check(a, s_redd, s_red);
+}
+
+// Filter prep only (initial centres, standalone assign).
+__global__ void __launch_bounds__(512) prep_filter_kernel(const double* c, float* w, float* cn, float* cmax,
+                                                          int k, int m, int mpad) {
+  __shared__ float s_red[32];
+  block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red);
+}
+
+// Standalone congruence test (km_converged).
+__global__ void __launch_bounds__(512) converged_kernel(const double* prev, const double* next, int k, int m,
+                                                        double tol, int* out) {
+  __shared__ double s_redd[32];
+  const int c = block_converged(prev, next, k, m, tol, s_redd);
+  if (threadIdx.x == 0) *out = c;
+}
+
+// ---------------------------------------------------------------------------
+// Empty-cluster repair (engine.py:265-276): d2_i = ‖x_i − C[label_i]‖² (fp64,
+// _kernels.self_distances_block :116-126); per empty cluster (ascending):
+// s = argmax d2 (first index), relabel s, move one count, C[c] = x_s, d2_s = 0.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void self_d2_kernel(const T* __restrict__ x, int64_t n, int m, const double* __restrict__ c,
+                               const int32_t* __restrict__ labels, double* __restrict__ d2) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d2[i] = exact_d2<T>(x + i * m, c + (size_t)labels[i] * m, m);
+}
+
+struct ArgMax { double v; long long i; };
+
+__device__ __forceinline__ ArgMax argmax_better(ArgMax a, ArgMax b) {
+  // larger value wins; equal values → lower index (np.argmax returns the first)
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+
+__global__ void argmax_partial_kernel(const double* __restrict__ d2, int64_t n, ArgMax* partial) {
+  ArgMax best{-1.0, (long long)n};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    best = argmax_better(best, ArgMax{d2[i], (long long)i});
+  __shared__ ArgMax s[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax other{__shfl_xor_sync(0xffffffffu, best.v, o), __shfl_xor_sync(0xffffffffu, best.i, o)};
+    best = argmax_better(best, other);
+  }
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = argmax_better(best, s[w]);
+    partial[blockIdx.x] = best;
+  }
+}
+
+// One thread: reduce the partials, apply the relabel for empty cluster `c`.
+template <typename T>
+__global__ void repair_apply_kernel(const ArgMax* partial, int nparts, int c, const T* __restrict__ x, int m,
+                                    int32_t* labels, double* d2, long long* model_counts, double* cur,
+                                    ArgMax* winner_out) {
+  if (threadIdx.x != 0) return;
+  ArgMax best = partial[0];
+  for (int i = 1; i < nparts; ++i) best = argmax_better(best, partial[i]);
+  const long long s = best.i;
+  const int donor = labels[s];
+  labels[s] = c;
+  model_counts[donor] -= 1;
+  model_counts[c] += 1;
+  for (int f = 0; f < m; ++f) cur[(size_t)c * m + f] = to_f64(x[s * m + f]);
+  d2[s] = 0.0;
+  if (winner_out) *winner_out = best;
+}
+
+// Local candidate only (multi-GPU repair: the caller picks the global winner).
+__global__ void argmax_final_kernel(const ArgMax* partial, int nparts, ArgMax* out) {
+  if (threadIdx.x != 0) return;
+  ArgMax best = partial[0];
+  for (int i = 1; i < nparts; ++i) best = argmax_better(best, partial[i]);
+  *out = best;
+}
+
+// Apply a repair decided across shards.
+__global__ void repair_apply_global_kernel(int c, int owner, long long local_row, const double* coords, int donor,
+                                           int m, int32_t* labels, double* d2, long long* model_counts,
+                                           double* cur) {
+  if (threadIdx.x != 0) return;
+  if (owner) {
+    labels[local_row] = c;
+    d2[local_row] = 0.0;
+  }
+  model_counts[donor] -= 1;
+  model_counts[c] += 1;
+  for (int f = 0; f < m; ++f) cur[(size_t)c * m + f] = coords[f];
+}
+
+// ---------------------------------------------------------------------------
+// Reporting neighbours of the hot path.
+// ---------------------------------------------------------------------------
+// wcss: Σ_i ‖x_i − C[label_i]‖² — each term exactly as _kernels.wcss_block,
+// the total accumulated in 2^-(F2) fixed point (exact integer adds, so the
+// total does not depend on the reduction order).
+template <typename T>
+__global__ void wcss_kernel(const T* __restrict__ x, int64_t n, int m, const double* __restrict__ c,
+                            const int32_t* __restrict__ labels, double scale, unsigned long long* out_hi_lo) {
+  long long acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double d = exact_d2<T>(x + i * m, c + (size_t)labels[i] * m, m);
+    acc += __double2ll_rn(__dmul_rn(d, scale));
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out_hi_lo, (unsigned long long)acc);
+}
+
+// transform: out[i,c] = sqrt(exact_d2(x_i, C_c))  (_kernels.center_distances :158-170)
+template <typename T>
+__global__ void center_distances_kernel(const T* __restrict__ x, int64_t n, int m, const double* __restrict__ c,
+                                        int k, double* __restrict__ out) {
+  const int64_t total = n * (int64_t)k;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = idx / k;
+    const int cc = (int)(idx - i * k);
+    out[idx] = sqrt(exact_d2<T>(x + i * m, c + (size_t)cc * m, m));
+  }
+}
+
+// max |x| (exact) for the fixed-point scale; flags[0] |= non-finite seen,
+// flags[1] |= value not exactly representable in fp32 (fp64 input only).
+template <typename T>
+__global__ void absmax_kernel(const T* __restrict__ x, int64_t count, unsigned long long* out_bits,
+                              int* flags) {
+  double mx = 0.0;
+  int bad = 0, inexact = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+    const double v = to_f64(x[i]);
+    if (!isfinite(v)) { bad = 1; continue; }
+    mx = fmax(mx, fabs(v));
+    if (sizeof(T) == 8 && (double)__double2float_rn(v) != v) inexact = 1;
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  bad = __any_sync(0xffffffffu, bad);
+  inexact = __any_sync(0xffffffffu, inexact);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(out_bits, (unsigned long long)__double_as_longlong(mx));
+    if (bad) atomicOr(flags, 1);
+    if (inexact) atomicOr(flags + 1, 1);
+  }
+}
+
+__global__ void narrow_f64_kernel(const double* __restrict__ in, int64_t count, float* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = __double2float_rn(in[i]);
+}
+
+// int32 labels → int64 (download path)
+__global__ void widen_labels_kernel(const int32_t* __restrict__ in, int64_t n, long long* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[i];
+}
+
+}  // namespace km
