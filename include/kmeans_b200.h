@@ -151,6 +151,13 @@ KM_API int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, 
 
 KM_API int km_get_stats(km_engine* e, km_stats* out);
 KM_API int km_reset_stats(km_engine* e);
+/* Kernel path for the fused pass: 0 = auto (tcgen05 tensor-core pass when the
+ * shape allows: fp32 points, m ≤ 31, k ≤ 64; SIMT otherwise), 1 = SIMT only,
+ * 2 = tensor core required (error if not available). */
+KM_API int km_set_kernel_path(km_engine* e, int32_t path);
+KM_API int km_kernel_path(km_engine* e, int32_t* out);   /* path the next pass uses: 1 SIMT, 2 tensor core */
+/* Test hook: raw tensor-core filter scores S~[n×k] = ‖c~‖² − 2x·c~ (fp32) for the given centres. */
+KM_API int km_debug_filter_scores(km_engine* e, const double* centers, int32_t k, float* out);
 /* Record a CUDA event pair around every fused pass km_lloyd launches (on the
  * handle's stream) and accumulate the device time of the passes that ran. */
 KM_API int km_set_profiling(km_engine* e, int32_t enable);

@@ -22,7 +22,11 @@ from .exceptions import (
     ValidationFailureError,
 )
 
+import os as _os
+
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libkmeans_b200.so"
+if _os.environ.get("KM_LIB_VARIANT"):  # tuning builds only (tools/); the product uses the default library
+    LIB_PATH = Path(__file__).resolve().parent / "_lib" / "variants" / f"libkmeans_b200_{_os.environ['KM_LIB_VARIANT']}.so"
 HEADER = Path(__file__).resolve().parent.parent / "include" / "kmeans_b200.h"
 
 KM_OK = 0
@@ -81,6 +85,9 @@ SIGNATURES = {
     "km_step_read": (ctypes.c_int, [P, P, P, P]),
     "km_get_stats": (ctypes.c_int, [P, ctypes.POINTER(KmStats)]),
     "km_reset_stats": (ctypes.c_int, [P]),
+    "km_set_kernel_path": (ctypes.c_int, [P, I32]),
+    "km_kernel_path": (ctypes.c_int, [P, ctypes.POINTER(I32)]),
+    "km_debug_filter_scores": (ctypes.c_int, [P, P, I32, P]),
     "km_set_profiling": (ctypes.c_int, [P, I32]),
 }
 
@@ -291,6 +298,21 @@ class NativeEngine:
 
     def set_profiling(self, enable: bool):
         self._check(self._lib.km_set_profiling(self._h, int(bool(enable))))
+
+    def set_kernel_path(self, path: int):
+        """0 = auto (tensor core when eligible), 1 = SIMT only, 2 = tensor core required."""
+        self._check(self._lib.km_set_kernel_path(self._h, int(path)))
+
+    def kernel_path(self) -> int:
+        out = I32(0)
+        self._check(self._lib.km_kernel_path(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    def debug_filter_scores(self, centers: np.ndarray) -> np.ndarray:
+        centers = np.ascontiguousarray(centers, dtype=np.float64)
+        out = np.empty((self.n, centers.shape[0]), dtype=np.float32)
+        self._check(self._lib.km_debug_filter_scores(self._h, _ptr(centers), centers.shape[0], _ptr(out)))
+        return out
 
     def reset_stats(self):
         self._check(self._lib.km_reset_stats(self._h))

@@ -35,7 +35,8 @@ def _nvcc() -> str:
 
 
 def _sources():
-    return sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "kmeans_b200.h"]
+    return (sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.h"))
+            + [ROOT / "include" / "kmeans_b200.h"])
 
 
 def _stale(target: Path, deps) -> bool:
@@ -45,27 +46,47 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps if d.exists())
 
 
-def build_engine(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale(LIB, _sources()):
-        return LIB
+def build_engine(force: bool = False, verbose: bool = False, defines=(), out: Path = None) -> Path:
+    """Compile every csrc/*.cu to an object in parallel, then link the shared library.
+
+    ``defines``/``out`` build a tuning variant (e.g. KM_WAIT_MODE=1) into another file.
+    """
+    lib = out or LIB
+    if not force and not _stale(lib, _sources()):
+        return lib
+    from concurrent.futures import ThreadPoolExecutor
+
     LIBDIR.mkdir(parents=True, exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [
-        _nvcc(), *NVCC_ARCH, "-O3", "-lineinfo", "-std=c++17",
-        "-Xptxas", "-v" if verbose else "-O3",
-        "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden",
-        "-shared", "-cudart", "static",
-        "-I", str(ROOT / "include"),
-        str(CSRC / "kmeans_engine.cu"),
-        "-o", str(tmp),
-    ]
+    objdir = LIBDIR / ("obj" if out is None else "obj_" + lib.stem)
+    objdir.mkdir(parents=True, exist_ok=True)
+    nvcc = _nvcc()
+    common = [nvcc, *NVCC_ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v" if verbose else "-O3",
+              "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden", "-I", str(ROOT / "include"),
+              *[f"-D{d}" for d in defines]]
+    units = sorted(CSRC.glob("*.cu"))
+
+    def compile_one(src: Path):
+        obj = objdir / (src.stem + ".o")
+        cmd = [*common, "-c", str(src), "-o", str(obj)]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+        return obj, res.stderr
+
+    with ThreadPoolExecutor(max_workers=len(units)) as pool:
+        results = list(pool.map(compile_one, units))
+    if verbose:
+        for _, err in results:
+            sys.stderr.write(err)
+    lib.parent.mkdir(parents=True, exist_ok=True)
+    tmp = lib.with_suffix(".so.tmp")
+    cmd = [nvcc, *NVCC_ARCH, "-shared", "-cudart", "static", "-Xcompiler", "-fPIC",
+           *[str(o) for o, _ in results], "-o", str(tmp)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
-    if verbose:
-        sys.stderr.write(res.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+        raise RuntimeError(f"link failed:\n{' '.join(cmd)}\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, lib)
+    return lib
 
 
 def build_oracle(force: bool = False) -> Path:

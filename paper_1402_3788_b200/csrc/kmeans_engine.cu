@@ -11,12 +11,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/kmeans_b200.h"
 #include "kmeans_kernels.cuh"
+#include "kmeans_tc.h"
 
 using namespace km;
 
@@ -61,6 +63,11 @@ struct km_engine {
   unsigned long long* scratch_u = nullptr;  // 2
   long long* labels64 = nullptr;    // n (download staging)
   int n_partials = 0;
+
+  float* wsplit = nullptr;          // [2][kp][32] tensor-core filter operand
+  int32_t kp = 0;                   // k rounded up to 16 (tensor-core N)
+  int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required
+  float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
 
   km_stats stats{};
   bool profiling = false;
@@ -122,10 +129,10 @@ static int mp_for(int m) {
 }
 
 static size_t pass_smem_bytes(const km_engine* e, bool assign, bool smem_acc, int elem_bytes) {
+  auto a16 = [](size_t v) { return (v + 15) & ~size_t(15); };
   size_t b = 0;
-  if (smem_acc) b += ((size_t)e->k * e->m + e->k) * 8;
-  if (assign) b += (size_t)e->k * e->mpad * 4 + (size_t)e->k * 4;
-  b = (b + 15) & ~size_t(15);
+  if (assign) b = a16(b + (size_t)e->k * e->mpad * 4) + 0, b = a16(b + (size_t)e->k * 4);
+  if (smem_acc) b = a16(b + ((size_t)e->k * e->m + e->k) * 8);
   b += (size_t)kTileRows * e->m * elem_bytes;
   return b;
 }
@@ -170,10 +177,89 @@ static int launch_pass_mp(km_engine* e, const PassArgs& a, size_t smem) {
 
 enum PassMode { PASS_ASSIGN_SUMS = 0, PASS_ASSIGN_ONLY = 1, PASS_SUMS_ONLY = 2 };
 
+// tensor-core path: fp32 resident points, m ≤ 31 (ones column + 8 bytes/feature fit
+// one 128 B row / two 128-row byte blocks), k ≤ 64 (3·KP TMEM columns, 2 CTAs/SM)
+static bool tc_eligible(const km_engine* e) {
+  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= 64;
+}
+static bool use_tc(const km_engine* e) { return e->path_pref != 1 && tc_eligible(e); }
+
+static int tc_mp_for(int m) { return m <= 7 ? 7 : m <= 15 ? 15 : m <= 23 ? 23 : 31; }
+
+static float host_err_coef_tc(int m, int mp) {
+  // |S_tc − S| ≤ coef·(‖x‖ + max‖c‖)²: FMA-chain/alignment error of the 3·KS tf32
+  // MMA steps + the dropped Xl·Wl term + tf32 truncation of the lo parts + the
+  // fp32 rounding of x, c, ‖c‖² + the reference's own fp64 rounding; ×2 safety.
+  // Measured worst case on B200 (tests/test_gpu_tensorcore.py): ≈ 6e-7 ≈ 10·2⁻²⁴ for every m;
+  // the coefficient below keeps ≥ 6× margin over it.
+  const int ks = (mp + 1 + 7) / 8;
+  return (float)std::max((m + 8 + 12 * ks) * std::ldexp(1.0, -23), std::ldexp(1.0, -18));
+}
+
+static int launch_tc(km_engine* e, bool do_sums, bool gated) {
+  tc::TcArgs a{};
+  a.x = (const float*)e->x;
+  a.n = e->n;
+  a.m = e->m;
+  a.k = e->k;
+  a.wsplit = e->wsplit;
+  a.cmax = e->cmax;
+  a.c64 = e->cur;
+  a.labels = e->labels;
+  a.part = e->part;
+  const int F = e->frac_bits;
+  a.scale_d = std::ldexp(1.0, F);
+  a.use_dscale = (F > 120 || F < -120) ? 1 : 0;
+  a.scale_f = a.use_dscale ? 1.0f : (float)std::ldexp(1.0, F);
+  const int mp = tc_mp_for(e->m);
+  a.err_coef = host_err_coef_tc(e->m, mp);
+  a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -140));
+  a.nx_inflate = (float)(1.0 + (e->m + 2) * std::ldexp(1.0, -24));
+  a.exact_only = (e->absmax > std::ldexp(1.0, 50)) ? 1 : 0;
+  a.st = e->st;
+  a.gate = gated ? 1 : 0;
+  a.do_sums = do_sums ? 1 : 0;
+  a.dbg_scores = e->dbg_scores;
+  a.dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
+  a.dbg_times = nullptr;
+  if (getenv("KM_TC_TIMES")) {  // tuning only: dump per-tile stamps of CTA 0 to a file after the pass
+    static long long* dt = nullptr;
+    if (!dt) cudaMalloc((void**)&dt, 64 * 8 * 8);
+    cudaMemsetAsync(dt, 0, 64 * 8 * 8, e->stream);
+    a.dbg_times = dt;
+  }
+  char msg[256] = {0};
+  cudaError_t c = cudaSuccess;
+  const int rc = tc::launch(a, mp, e->kp, e->num_sms, e->smem_optin, e->stream, &c, msg, sizeof msg);
+  if (rc == 1) return cuda_fail(e, c, msg);
+  if (rc == 2) return set_err(e, KM_ERR_CAPACITY, "%s", msg);
+  e->stats.kernel_launches += 1;
+  if (a.dbg_times) {
+    long long h[64 * 8];
+    cudaMemcpyAsync(h, a.dbg_times, sizeof h, cudaMemcpyDeviceToHost, e->stream);
+    cudaStreamSynchronize(e->stream);
+    FILE* f = fopen(getenv("KM_TC_TIMES"), "a");
+    if (f) {
+      for (int i = 0; i < 64; ++i) {
+        if (!h[i * 8]) continue;
+        fprintf(f, "tile %2d", i);
+        for (int q = 1; q < 7; ++q) fprintf(f, " %6lld", h[i * 8 + q] - h[i * 8 + q - 1]);
+        fprintf(f, "  | start %lld\n", h[i * 8] - h[0]);
+      }
+      fprintf(f, "----\n");
+      fclose(f);
+    }
+  }
+  return KM_OK;
+}
+
 static float host_err_coef(int m) { return (float)((m + 8) * std::ldexp(1.0, -24) * 1.25); }
 
 static int launch_pass(km_engine* e, PassMode mode, bool gated) {
   if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (mode != PASS_SUMS_ONLY && use_tc(e)) return launch_tc(e, mode == PASS_ASSIGN_SUMS, gated);
+  if (e->path_pref == 2) return set_err(e, KM_ERR_CAPACITY, "tensor-core path not available for m=%d k=%d (%d-byte points)",
+                                        e->m, e->k, e->point_bytes);
   const bool A = mode != PASS_SUMS_ONLY;
   PassArgs a{};
   a.x = e->x;
@@ -227,6 +313,8 @@ static FinishArgs finish_args(km_engine* e, int mode) {
   f.w = e->w;
   f.cn = e->cn;
   f.cmax = e->cmax;
+  f.wsplit = tc_eligible(e) ? e->wsplit : nullptr;
+  f.kp = e->kp;
   f.k = e->k;
   f.m = e->m;
   f.mpad = e->mpad;
@@ -260,8 +348,8 @@ static int launch_check(km_engine* e) {
 }
 
 static int launch_prep(km_engine* e) {
-  prep_filter_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(e->cur, e->w, e->cn, e->cmax, e->k, e->m,
-                                                                      e->mpad);
+  prep_filter_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(
+      e->cur, e->w, e->cn, e->cmax, e->k, e->m, e->mpad, tc_eligible(e) ? e->wsplit : nullptr, e->kp);
   CK_LAUNCH("prep_filter_kernel launch");
   e->stats.kernel_launches += 1;
   return KM_OK;
@@ -295,11 +383,12 @@ static int grid_for(km_engine* e, int64_t n, int per_sm = 8) {
 static void free_k(km_engine* e) {
   dfree(e->labels); dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
   dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->d2); dfree(e->partials); dfree(e->winner);
-  dfree(e->scratch_d); dfree(e->labels64);
+  dfree(e->scratch_d); dfree(e->labels64); dfree(e->wsplit);
   e->labels = nullptr; e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
   e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->d2 = nullptr; e->partials = nullptr; e->winner = nullptr;
-  e->scratch_d = nullptr; e->labels64 = nullptr;
+  e->scratch_d = nullptr; e->labels64 = nullptr; e->wsplit = nullptr;
   e->k = 0;
+  e->kp = 0;
 }
 
 static int ensure_k(km_engine* e, int32_t k) {
@@ -322,6 +411,9 @@ static int ensure_k(km_engine* e, int32_t k) {
   e->n_partials = grid_for(e, e->n);
   if ((r = dalloc(e, &e->partials, sizeof(ArgMax) * (size_t)e->n_partials))) return r;
   if ((r = dalloc(e, &e->winner, sizeof(ArgMax)))) return r;
+  e->kp = (k + 15) & ~15;
+  if ((r = dalloc(e, &e->wsplit, sizeof(float) * 2 * 32 * (size_t)e->kp))) return r;
+  CK(cudaMemsetAsync(e->wsplit, 0, sizeof(float) * 2 * 32 * (size_t)e->kp, e->stream));
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * m + k), e->stream));
   CK(cudaMemsetAsync(e->labels, 0, sizeof(int32_t) * (size_t)e->n, e->stream));
   e->k = k;
@@ -1022,6 +1114,47 @@ int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, int64_t
   if (counts_out) CK(cudaMemcpyAsync(counts_out, e->model_counts, 8 * (size_t)e->k, cudaMemcpyDeviceToHost, e->stream));
   if (labels_out && (r = download_labels(e, labels_out))) return r;
   CK(cudaStreamSynchronize(e->stream));
+  return KM_OK;
+}
+
+int km_set_kernel_path(km_engine* e, int32_t path) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (path < 0 || path > 2) return set_err(e, KM_ERR_CONTRACT, "path must be 0 (auto), 1 (SIMT) or 2 (tensor core)");
+  e->path_pref = path;
+  return KM_OK;
+}
+
+int km_kernel_path(km_engine* e, int32_t* out) {
+  if (!e || !out) return set_err(e, KM_ERR_CONTRACT, "null argument");
+  *out = use_tc(e) ? 2 : 1;
+  return KM_OK;
+}
+
+int km_debug_filter_scores(km_engine* e, const double* centers, int32_t k, float* out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (!out) return set_err(e, KM_ERR_CONTRACT, "null out");
+  if ((r = check_centers(e, centers, k))) return r;
+  if ((r = ensure_k(e, k))) return r;
+  if (!use_tc(e)) return set_err(e, KM_ERR_CAPACITY, "tensor-core filter not available for this shape");
+  float* dbg = nullptr;
+  if ((r = dalloc(e, &dbg, sizeof(float) * (size_t)e->n * k))) return r;
+  CK(cudaMemcpyAsync(e->cur, centers, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
+  if ((r = reset_state(e, 1, 0.0))) { cudaFree(dbg); return r; }
+  if ((r = launch_prep(e))) { cudaFree(dbg); return r; }
+  CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  e->dbg_scores = dbg;
+  r = launch_pass(e, PASS_ASSIGN_ONLY, false);
+  e->dbg_scores = nullptr;
+  cudaError_t c = cudaSuccess;
+  if (!r) c = cudaMemcpyAsync(out, dbg, sizeof(float) * (size_t)e->n * k, cudaMemcpyDeviceToHost, e->stream);
+  if (!r && c == cudaSuccess) c = cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream);
+  if (!r && c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
+  cudaFree(dbg);
+  if (r) return r;
+  if (c != cudaSuccess) return cuda_fail(e, c, "km_debug_filter_scores");
   return KM_OK;
 }
 

@@ -24,24 +24,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "kmeans_state.h"
+
 namespace km {
 
 constexpr int kTileRows = 256;   // rows per CTA tile == threads per CTA
 constexpr int kThreads = 256;
 
-// Device-side loop state (lives in device memory, mirrored to pinned host).
-struct DevState {
-  int32_t t;          // updates performed (reference `iterations`)
-  int32_t done;       // loop finished
-  int32_t converged;  // finished by convergence
-  int32_t exhausted;  // t == max_iters without convergence: one more assign pass, then done
-  int32_t need_host;  // empty clusters: host must run the repair before the check
-  int32_t n_empty;
-  int32_t max_iters;
-  int32_t bad_label;  // first invalid label seen by a sums-only pass (+1), 0 = none
-  unsigned long long rechecked;
-  double tol;
-};
 
 struct PassArgs {
   const void* x;          // n × m row-major, T = float or double
@@ -144,13 +133,16 @@ __global__ void __launch_bounds__(kThreads) lloyd_pass_kernel(PassArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int m = a.m, k = a.k, tid = threadIdx.x;
   const int mpad = a.mpad;
-  // layout: [acc k*m u64][cnt k u64][w k*mpad f32][cn k f32][tile 256*m T]
-  unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(smem);
+  // layout (16 B aligned sections): [w k*mpad f32][cn k f32][acc k*m u64][cnt k u64][tile 256*m T]
+  auto align16 = [](size_t v) { return (v + 15) & ~size_t(15); };
+  size_t off = 0;
+  float* s_w = reinterpret_cast<float*>(smem + off);
+  off = align16(off + (DO_ASSIGN ? (size_t)k * mpad * 4 : 0));
+  float* s_cn = reinterpret_cast<float*>(smem + off);
+  off = align16(off + (DO_ASSIGN ? (size_t)k * 4 : 0));
+  unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(smem + off);
   unsigned long long* s_cnt = s_acc + (SMEM_ACC ? (size_t)k * m : 0);
-  float* s_w = reinterpret_cast<float*>(s_cnt + (SMEM_ACC ? k : 0));
-  float* s_cn = s_w + (DO_ASSIGN ? (size_t)k * mpad : 0);
-  size_t off = reinterpret_cast<unsigned char*>(s_cn + (DO_ASSIGN ? k : 0)) - smem;
-  off = (off + 15) & ~size_t(15);
+  off = align16(off + (SMEM_ACC ? ((size_t)k * m + k) * 8 : 0));
   T* s_tile = reinterpret_cast<T*>(smem + off);
 
   if (SMEM_ACC) {
@@ -288,6 +280,8 @@ struct FinishArgs {
   float* w;                  // k × mpad (out: −2·fl32(C_t))
   float* cn;                 // k
   float* cmax;               // [0]
+  float* wsplit;             // [2][kp][32] tensor-core filter operand (nullable)
+  int32_t kp;
   int32_t k, m, mpad;
   double inv_scale;          // 2^-F
   DevState* st;
@@ -295,7 +289,30 @@ struct FinishArgs {
 };
 
 __device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, float* w, float* cn, float* cmax,
-                                                  int k, int m, int mpad, float* s_red) {
+                                                  int k, int m, int mpad, float* s_red, float* wsplit = nullptr,
+                                                  int kp = 0) {
+  // tensor-core operand W~ (hi/lo tf32 split): rows c < k = (−2·fl32(c_f), f < m; ‖fl32(c)‖² at f = m)
+  if (wsplit != nullptr) {
+    for (int i = threadIdx.x; i < kp * 32; i += blockDim.x) {
+      const int cc = i >> 5, f = i & 31;
+      float v = 0.f;
+      if (cc < k) {
+        if (f < m) {
+          v = -2.0f * __double2float_rn(c[(size_t)cc * m + f]);
+        } else if (f == m) {
+          double s = 0.0;
+          for (int g = 0; g < m; ++g) {
+            const double e = (double)__double2float_rn(c[(size_t)cc * m + g]);
+            s = __fma_rn(e, e, s);
+          }
+          v = __double2float_rn(s);
+        }
+      }
+      const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
+      wsplit[i] = h;
+      wsplit[kp * 32 + i] = v - h;
+    }
+  }
   // w = −2·fl32(c) (exact scaling), cn = fl32(Σ fl32(c)²), cmax = max √(Σ fl32(c)²) rounded up.
   for (int i = threadIdx.x; i < k * mpad; i += blockDim.x) {
     const int cc = i / mpad, f = i - cc * mpad;
@@ -348,7 +365,7 @@ __device__ __forceinline__ int block_converged(const double* __restrict__ prev, 
 __device__ __forceinline__ void loop_check(FinishArgs& a, double* s_redd, float* s_red) {
   DevState* st = a.st;
   const int conv = block_converged(a.prev, a.cur, a.k, a.m, st->tol, s_redd);
-  block_prep_filter(a.cur, a.w, a.cn, a.cmax, a.k, a.m, a.mpad, s_red);
+  block_prep_filter(a.cur, a.w, a.cn, a.cmax, a.k, a.m, a.mpad, s_red, a.wsplit, a.kp);
   if (threadIdx.x == 0) {
     st->need_host = 0;
     if (conv) {
@@ -425,9 +442,9 @@ __global__ void __launch_bounds__(512) lloyd_check_kernel(FinishArgs a) {
 
 // Filter prep only (initial centres, standalone assign).
 __global__ void __launch_bounds__(512) prep_filter_kernel(const double* c, float* w, float* cn, float* cmax,
-                                                          int k, int m, int mpad) {
+                                                          int k, int m, int mpad, float* wsplit, int kp) {
   __shared__ float s_red[32];
-  block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red);
+  block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red, wsplit, kp);
 }
 
 // Standalone congruence test (km_converged).

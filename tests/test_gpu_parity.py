@@ -217,12 +217,17 @@ def test_full_size_properties(native, n, m, k, iters):
     rows = np.random.default_rng(0).choice(n, size=20_000, replace=False)
     ref_labels, _ = oracle.assign(x[rows].astype(np.float64), centers)
     assert np.array_equal(labels[rows], ref_labels)
-    # one more update on the device vs fp64 means
+    # one more update on the device vs fp64 means of the pre-repair labels
+    # (repaired clusters take a sample's coordinates; donor centres are not
+    # recomputed — engine.py:265-276)
     lab = labels.copy()
     c_next, cnt_next = eng.update(lab, k)
     xd = x.astype(np.float64)
+    before = np.bincount(labels, minlength=k)
+    occ = before > 0
     for f in range(m):
-        s = np.bincount(lab, weights=xd[:, f], minlength=k)
-        occ = cnt_next > 0
-        assert rel_err(c_next[occ, f], s[occ] / cnt_next[occ]) <= 1e-12
+        s = np.bincount(labels, weights=xd[:, f], minlength=k)
+        assert rel_err(c_next[occ, f], s[occ] / before[occ]) <= 1e-12
+    for c in np.flatnonzero(~occ):  # repaired: centre = the relabelled sample
+        assert np.array_equal(c_next[c], xd[np.flatnonzero(lab == c)[0]])
     eng.close()

@@ -1,0 +1,78 @@
+"""tcgen05 fused pass: the certified error bound of the 3xTF32 tensor-core
+filter holds on real hardware, and the tensor-core and SIMT kernels return
+bit-identical results (both must equal the reference)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def native():
+    from paper_1402_3788_b200 import _native
+
+    return _native
+
+
+def exact_scores(x, c):
+    """‖c~‖² − 2 x·c~ in fp64 with c~ = fl32(c) (what the filter approximates), plus per-point ‖x‖."""
+    cf = c.astype(np.float32).astype(np.float64)
+    xd = x.astype(np.float64)
+    return (cf * cf).sum(1)[None, :] - 2.0 * xd @ cf.T
+
+
+@pytest.mark.parametrize("n,m,k", [(200_000, 25, 16), (100_000, 10, 8), (50_000, 5, 4), (60_000, 31, 64),
+                                   (30_000, 23, 40), (10_000, 1, 3)])
+def test_filter_error_within_certified_bound(n, m, k):
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(n, m, k, seed=11, dtype=np.float32)
+    c = x[:k].astype(np.float64) + 0.37  # centres not on data points
+    eng = native().NativeEngine(0)
+    eng.load(x)
+    assert eng.kernel_path() in (1, 2)
+    got = eng.debug_filter_scores(c)
+    eng.close()
+    want = exact_scores(x, c)
+    nx = np.sqrt((x.astype(np.float64) ** 2).sum(1))
+    cmax = np.sqrt((c.astype(np.float32).astype(np.float64) ** 2).sum(1)).max()
+    scale = (nx + cmax) ** 2
+    mp = 7 if m <= 7 else 15 if m <= 15 else 23 if m <= 23 else 31
+    ks = (mp + 1 + 7) // 8
+    coef = max((m + 8 + 12 * ks) * 2.0 ** -23, 2.0 ** -18)
+    ratio = np.abs(got - want) / scale[:, None]
+    worst = float(ratio.max())
+    print(f"n={n} m={m} k={k}: max |S_tc - S| / (|x|+C)^2 = {worst:.3e}, certified coef = {coef:.3e}, "
+          f"margin {coef / max(worst, 1e-30):.1f}x")
+    assert worst <= coef / 4, "tensor-core filter error too close to (or above) its certified bound"
+
+
+@pytest.mark.parametrize("name", ["synth_10k_5_4", "synth_20k_25_16", "synth_30k_10_8"])
+def test_tensorcore_and_simt_agree(name):
+    g = golden(name)
+    out = {}
+    for path in (1, 2):
+        eng = native().NativeEngine(0)
+        eng.load(g["coords"])
+        eng.set_kernel_path(path)
+        out[path] = eng.lloyd(g["c0"], int(g["max_iters"]), float(g["tol"]))
+        assert eng.kernel_path() == path
+        eng.close()
+    a, b = out[1], out[2]
+    assert a[3] == b[3] == int(g["iterations"])
+    assert np.array_equal(a[2], b[2]) and np.array_equal(a[2], g["labels"].astype(np.int64))
+    assert np.array_equal(a[0], b[0])  # same exact integer sums → bit-identical centres
+    assert np.array_equal(a[1], b[1])
+
+
+def test_headline_shape_uses_tensor_cores():
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(4096, 25, 16, seed=0, dtype=np.float32)
+    eng = native().NativeEngine(0)
+    eng.load(x)
+    eng.lloyd(x[:16].astype(np.float64), 2, 0.0)
+    assert eng.kernel_path() == 2
+    eng.close()
