@@ -61,6 +61,7 @@ typedef struct km_stats {
   int32_t frac_bits;       /* fixed-point fraction bits F of the cluster sums  */
   int32_t point_bytes;     /* 4 (fp32 resident points) or 8 (fp64)            */
   int64_t kernel_launches; /* kernels this handle launched (cumulative)       */
+  int64_t changed;         /* labels changed by incremental passes (last run) */
   int64_t pass_timed;      /* fused passes timed with CUDA events (profiling) */
   double pass_ms_total;    /* their summed device time, ms                    */
 } km_stats;
@@ -144,6 +145,9 @@ KM_API int km_step_repair_prepare(km_engine* e);                 /* self-distanc
 KM_API int km_step_repair_candidate(km_engine* e, double* d2_out, int64_t* row_out, double* coords_out);
 KM_API int km_step_repair_apply(km_engine* e, int32_t empty_cluster, int32_t owner_is_me,
                          int64_t local_row, const double* coords, int32_t donor_cluster_or_neg);
+/* exhausted run: after the final pass and its allreduce, fold it into the
+ * totals so km_step_read returns counts = bincount(L_T) */
+KM_API int km_step_fold(km_engine* e);
 KM_API int km_step_empty_list(km_engine* e, int32_t* empties_out, int32_t* n_out);
 KM_API int km_step_label_of(km_engine* e, int64_t local_row, int32_t* label_out);
 KM_API int km_step_check(km_engine* e, double tol, int32_t* converged_out);

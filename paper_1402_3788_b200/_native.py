@@ -47,8 +47,8 @@ F64 = ctypes.c_double
 
 class KmStats(ctypes.Structure):
     _fields_ = [("passes", I64), ("rechecked", I64), ("repairs", I64), ("host_syncs", I64),
-                ("frac_bits", I32), ("point_bytes", I32), ("kernel_launches", I64), ("pass_timed", I64),
-                ("pass_ms_total", F64)]
+                ("frac_bits", I32), ("point_bytes", I32), ("kernel_launches", I64), ("changed", I64),
+                ("pass_timed", I64), ("pass_ms_total", F64)]
 
 
 # name -> (restype, argtypes); must list every symbol declared in the header
@@ -79,6 +79,7 @@ SIGNATURES = {
     "km_step_repair_prepare": (ctypes.c_int, [P]),
     "km_step_repair_candidate": (ctypes.c_int, [P, ctypes.POINTER(F64), ctypes.POINTER(I64), P]),
     "km_step_repair_apply": (ctypes.c_int, [P, I32, I32, I64, P, I32]),
+    "km_step_fold": (ctypes.c_int, [P]),
     "km_step_empty_list": (ctypes.c_int, [P, P, ctypes.POINTER(I32)]),
     "km_step_label_of": (ctypes.c_int, [P, I64, ctypes.POINTER(I32)]),
     "km_step_check": (ctypes.c_int, [P, F64, ctypes.POINTER(I32)]),
@@ -257,6 +258,9 @@ class NativeEngine:
         st = np.zeros(2, dtype=np.int32)
         self._check(self._lib.km_step_finish(self._h, float(tol), _ptr(st)))
         return int(st[0]), bool(st[1])
+
+    def step_fold(self):
+        self._check(self._lib.km_step_fold(self._h))
 
     def step_repair_prepare(self):
         self._check(self._lib.km_step_repair_prepare(self._h))

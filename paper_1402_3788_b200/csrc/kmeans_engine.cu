@@ -64,8 +64,12 @@ struct km_engine {
   long long* labels64 = nullptr;    // n (download staging)
   int n_partials = 0;
 
-  float* wsplit = nullptr;          // [2][kp][32] tensor-core filter operand
-  int32_t kp = 0;                   // k rounded up to 16 (tensor-core N)
+  unsigned short* wop = nullptr;    // [2kp][64] fp16 tensor-core B operand ([wh|wh], [wl|0])
+  int32_t kp = 0;                   // k padded for the tensor-core N dimension (16..128)
+  float pre = 1.f;                  // power-of-two prescale of the tensor-core operands
+  unsigned long long* tot = nullptr;  // running per-cluster totals (k·m sums + k counts)
+  bool next_full = true;            // next TC pass must add every point (no valid previous labels)
+  bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
   int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required
   float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
 
@@ -177,10 +181,10 @@ static int launch_pass_mp(km_engine* e, const PassArgs& a, size_t smem) {
 
 enum PassMode { PASS_ASSIGN_SUMS = 0, PASS_ASSIGN_ONLY = 1, PASS_SUMS_ONLY = 2 };
 
-// tensor-core path: fp32 resident points, m ≤ 31 (ones column + 8 bytes/feature fit
-// one 128 B row / two 128-row byte blocks), k ≤ 64 (3·KP TMEM columns, 2 CTAs/SM)
+// tensor-core path: fp32 resident points, m ≤ 31 ([xh|xl] + the ones column fit one 128-byte
+// fp16 row), k ≤ 128 (N = 2·KP ≤ 256 per MMA; 2 warpgroups × 2·KP TMEM columns ≤ 512)
 static bool tc_eligible(const km_engine* e) {
-  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= 64;
+  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= 128;
 }
 static bool use_tc(const km_engine* e) { return e->path_pref != 1 && tc_eligible(e); }
 
@@ -196,29 +200,30 @@ static float host_err_coef_tc(int m, int mp) {
   return (float)std::max((m + 8 + 12 * ks) * std::ldexp(1.0, -23), std::ldexp(1.0, -18));
 }
 
-static int launch_tc(km_engine* e, bool do_sums, bool gated) {
+static int launch_tc(km_engine* e, bool full, bool gated) {
   tc::TcArgs a{};
   a.x = (const float*)e->x;
   a.n = e->n;
   a.m = e->m;
   a.k = e->k;
-  a.wsplit = e->wsplit;
+  a.wop = e->wop;
   a.cmax = e->cmax;
   a.c64 = e->cur;
   a.labels = e->labels;
   a.part = e->part;
+  a.pre = e->pre;
   const int F = e->frac_bits;
   a.scale_d = std::ldexp(1.0, F);
   a.use_dscale = (F > 120 || F < -120) ? 1 : 0;
   a.scale_f = a.use_dscale ? 1.0f : (float)std::ldexp(1.0, F);
   const int mp = tc_mp_for(e->m);
   a.err_coef = host_err_coef_tc(e->m, mp);
-  a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -140));
+  a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -22));
   a.nx_inflate = (float)(1.0 + (e->m + 2) * std::ldexp(1.0, -24));
   a.exact_only = (e->absmax > std::ldexp(1.0, 50)) ? 1 : 0;
+  a.full = full ? 1 : 0;
   a.st = e->st;
   a.gate = gated ? 1 : 0;
-  a.do_sums = do_sums ? 1 : 0;
   a.dbg_scores = e->dbg_scores;
   a.dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
   a.dbg_times = nullptr;
@@ -257,7 +262,16 @@ static float host_err_coef(int m) { return (float)((m + 8) * std::ldexp(1.0, -24
 
 static int launch_pass(km_engine* e, PassMode mode, bool gated) {
   if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
-  if (mode != PASS_SUMS_ONLY && use_tc(e)) return launch_tc(e, mode == PASS_ASSIGN_SUMS, gated);
+  if (mode != PASS_SUMS_ONLY && use_tc(e)) {
+    // the TC pass updates the sums by exact deltas against the previous labels; the first
+    // pass of a run (and any standalone assign) adds every point
+    const bool full = e->next_full || mode == PASS_ASSIGN_ONLY;
+    const int r = launch_tc(e, full, gated);
+    if (!r && mode == PASS_ASSIGN_SUMS) e->next_full = false;  // tot will track the labels from here on
+    e->last_pass_full = full;
+    return r;
+  }
+  e->last_pass_full = true;  // SIMT passes recompute the sums
   if (e->path_pref == 2) return set_err(e, KM_ERR_CAPACITY, "tensor-core path not available for m=%d k=%d (%d-byte points)",
                                         e->m, e->k, e->point_bytes);
   const bool A = mode != PASS_SUMS_ONLY;
@@ -304,17 +318,20 @@ static int launch_pass(km_engine* e, PassMode mode, bool gated) {
   }
 }
 
-static FinishArgs finish_args(km_engine* e, int mode) {
+static FinishArgs finish_args(km_engine* e, int mode, bool accumulate) {
   FinishArgs f{};
   f.part = e->part;
+  f.tot = e->tot;
+  f.accumulate = accumulate ? 1 : 0;
   f.cur = e->cur;
   f.prev = e->prev;
   f.model_counts = e->model_counts;
   f.w = e->w;
   f.cn = e->cn;
   f.cmax = e->cmax;
-  f.wsplit = tc_eligible(e) ? e->wsplit : nullptr;
+  f.wop = tc_eligible(e) ? e->wop : nullptr;
   f.kp = e->kp;
+  f.pre = e->pre;
   f.k = e->k;
   f.m = e->m;
   f.mpad = e->mpad;
@@ -331,8 +348,8 @@ static int finish_threads(int k, int m) {
   return t;
 }
 
-static int launch_finish(km_engine* e, int mode) {
-  FinishArgs f = finish_args(e, mode);
+static int launch_finish(km_engine* e, int mode, bool accumulate) {
+  FinishArgs f = finish_args(e, mode, accumulate);
   lloyd_finish_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(f);
   CK_LAUNCH("lloyd_finish_kernel launch");
   e->stats.kernel_launches += 1;
@@ -340,7 +357,7 @@ static int launch_finish(km_engine* e, int mode) {
 }
 
 static int launch_check(km_engine* e) {
-  FinishArgs f = finish_args(e, 0);
+  FinishArgs f = finish_args(e, 0, false);
   lloyd_check_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(f);
   CK_LAUNCH("lloyd_check_kernel launch");
   e->stats.kernel_launches += 1;
@@ -349,7 +366,7 @@ static int launch_check(km_engine* e) {
 
 static int launch_prep(km_engine* e) {
   prep_filter_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(
-      e->cur, e->w, e->cn, e->cmax, e->k, e->m, e->mpad, tc_eligible(e) ? e->wsplit : nullptr, e->kp);
+      e->cur, e->w, e->cn, e->cmax, e->k, e->m, e->mpad, tc_eligible(e) ? e->wop : nullptr, e->kp, e->pre);
   CK_LAUNCH("prep_filter_kernel launch");
   e->stats.kernel_launches += 1;
   return KM_OK;
@@ -383,10 +400,10 @@ static int grid_for(km_engine* e, int64_t n, int per_sm = 8) {
 static void free_k(km_engine* e) {
   dfree(e->labels); dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
   dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->d2); dfree(e->partials); dfree(e->winner);
-  dfree(e->scratch_d); dfree(e->labels64); dfree(e->wsplit);
+  dfree(e->scratch_d); dfree(e->labels64); dfree(e->wop); dfree(e->tot);
   e->labels = nullptr; e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
   e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->d2 = nullptr; e->partials = nullptr; e->winner = nullptr;
-  e->scratch_d = nullptr; e->labels64 = nullptr; e->wsplit = nullptr;
+  e->scratch_d = nullptr; e->labels64 = nullptr; e->wop = nullptr; e->tot = nullptr;
   e->k = 0;
   e->kp = 0;
 }
@@ -411,9 +428,12 @@ static int ensure_k(km_engine* e, int32_t k) {
   e->n_partials = grid_for(e, e->n);
   if ((r = dalloc(e, &e->partials, sizeof(ArgMax) * (size_t)e->n_partials))) return r;
   if ((r = dalloc(e, &e->winner, sizeof(ArgMax)))) return r;
-  e->kp = (k + 15) & ~15;
-  if ((r = dalloc(e, &e->wsplit, sizeof(float) * 2 * 32 * (size_t)e->kp))) return r;
-  CK(cudaMemsetAsync(e->wsplit, 0, sizeof(float) * 2 * 32 * (size_t)e->kp, e->stream));
+  e->kp = k <= 64 ? ((k + 15) & ~15) : ((k + 31) & ~31);
+  if ((r = dalloc(e, &e->wop, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp))) return r;
+  CK(cudaMemsetAsync(e->wop, 0, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp, e->stream));
+  if ((r = dalloc(e, &e->tot, 8 * ((size_t)k * m + k)))) return r;
+  CK(cudaMemsetAsync(e->tot, 0, 8 * ((size_t)k * m + k), e->stream));
+  e->next_full = true;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * m + k), e->stream));
   CK(cudaMemsetAsync(e->labels, 0, sizeof(int32_t) * (size_t)e->n, e->stream));
   e->k = k;
@@ -456,6 +476,13 @@ static int scan_points(km_engine* e, const void* x, int bytes_per, int64_t count
 
 static int after_points_loaded(km_engine* e) {
   if (!e->frac_user) e->frac_bits = compute_frac_bits(e->absmax, e->n);
+  // tensor-core operand prescale 2^s: |x·2^s| < 1 (exact power of two)
+  e->pre = 1.f;
+  if (e->absmax > 0.0 && e->absmax < std::ldexp(1.0, 100)) {
+    const int s = -(std::ilogb(e->absmax) + 1);
+    e->pre = (float)std::ldexp(1.0, std::max(-120, std::min(120, s)));
+  }
+  e->next_full = true;
   e->stats.frac_bits = e->frac_bits;
   e->stats.point_bytes = e->point_bytes;
   return KM_OK;
@@ -513,11 +540,13 @@ static int repair_local(km_engine* e) {
     argmax_partial_kernel<<<e->n_partials, 256, 0, e->stream>>>(e->d2, e->n, e->partials);
     CK_LAUNCH("argmax_partial_kernel");
     if (e->point_bytes == 4)
-      repair_apply_kernel<float><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const float*)e->x, e->m,
-                                                          e->labels, e->d2, e->model_counts, e->cur, e->winner);
+      repair_apply_kernel<float><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const float*)e->x, e->k,
+                                                          e->m, e->labels, e->d2, e->model_counts, e->cur, e->tot,
+                                                          std::ldexp(1.0, e->frac_bits), e->winner);
     else
-      repair_apply_kernel<double><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const double*)e->x, e->m,
-                                                           e->labels, e->d2, e->model_counts, e->cur, e->winner);
+      repair_apply_kernel<double><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const double*)e->x,
+                                                           e->k, e->m, e->labels, e->d2, e->model_counts, e->cur,
+                                                           e->tot, std::ldexp(1.0, e->frac_bits), e->winner);
     CK_LAUNCH("repair_apply_kernel");
     e->stats.repairs += 1;
     e->stats.kernel_launches += 2;
@@ -756,7 +785,8 @@ int km_update(km_engine* e, int64_t* labels_inout, int32_t k, double* centers_ou
   if ((r = reset_state(e, 1, 0.0))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   if ((r = launch_pass(e, PASS_SUMS_ONLY, false))) return r;
-  if ((r = launch_finish(e, 1))) return r;
+  if ((r = launch_finish(e, 1, false))) return r;
+  e->next_full = true;
   if ((r = read_state(e))) return r;
   if (e->st_host->bad_label) return set_err(e, KM_ERR_VALIDATION, "label out of range [0, %d) on device", k);
   const bool repaired = e->st_host->n_empty > 0;
@@ -811,10 +841,16 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
   if ((r = reset_state(e, max_iters, tol))) return r;
   if ((r = launch_prep(e))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  e->next_full = true;  // the labels buffer does not hold L of this run yet
+  bool prev_full = true;
   int batch = 1;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
   auto timed_pass = [&](void) -> int {
-    if (!e->profiling) return launch_pass(e, PASS_ASSIGN_SUMS, true);
+    if (!e->profiling) {
+      const int rr = launch_pass(e, PASS_ASSIGN_SUMS, true);
+      prev_full = e->last_pass_full;
+      return rr;
+    }
     const size_t need = 2 * (timed.size() + 1);
     while (e->ev.size() < need) {
       cudaEvent_t ev;
@@ -825,6 +861,7 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
     CK(cudaEventRecord(a, e->stream));
     int rr = launch_pass(e, PASS_ASSIGN_SUMS, true);
     if (rr) return rr;
+    prev_full = e->last_pass_full;
     CK(cudaEventRecord(b, e->stream));
     timed.push_back({a, b});
     return KM_OK;
@@ -847,7 +884,7 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
   int t_before = 0;
   for (;;) {
     for (int b = 0; b < batch; ++b) {
-      if ((r = launch_finish(e, 0))) return r;
+      if ((r = launch_finish(e, 0, !prev_full))) return r;
       if ((r = timed_pass())) return r;
     }
     if ((r = read_state(e))) return r;
@@ -874,11 +911,10 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
   const DevState s = *e->st_host;
   e->stats.passes += 1 + s.t - (s.converged ? 1 : 0);
   e->stats.rechecked = (int64_t)s.rechecked;
+  e->stats.changed = (int64_t)s.changed;
   if (centers_out) CK(cudaMemcpyAsync(centers_out, e->cur, 8 * (size_t)k * e->m, cudaMemcpyDeviceToHost, e->stream));
-  if (counts_out) {
-    const void* src = s.converged ? (const void*)e->model_counts : (const void*)(e->part + (size_t)k * e->m);
-    CK(cudaMemcpyAsync(counts_out, src, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
-  }
+  if (counts_out)  // converged: counts of the update; exhausted: the final finish folded bincount(L_T)
+    CK(cudaMemcpyAsync(counts_out, e->model_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
   if (labels_out && (r = download_labels(e, labels_out))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   CK(cudaStreamSynchronize(e->stream));
@@ -976,6 +1012,7 @@ int km_step_begin(km_engine* e, const double* c0, int32_t k) {
   if ((r = reset_state(e, INT32_MAX, 0.0))) return r;
   if ((r = launch_prep(e))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
+  e->next_full = true;
   CK(cudaStreamSynchronize(e->stream));
   return KM_OK;
 }
@@ -1014,12 +1051,28 @@ int km_step_finish(km_engine* e, double tol, int32_t* status_out) {
   e->st_host->tol = tol;
   e->st_host->max_iters = INT32_MAX;
   CK(cudaMemcpyAsync(e->st, e->st_host, sizeof(DevState), cudaMemcpyHostToDevice, e->stream));
-  if ((r = launch_finish(e, 0))) return r;
+  if ((r = launch_finish(e, 0, !e->last_pass_full))) return r;
   if ((r = read_state(e))) return r;
   if (status_out) {
     status_out[0] = e->st_host->n_empty;
     status_out[1] = e->st_host->converged;
   }
+  return KM_OK;
+}
+
+int km_step_fold(km_engine* e) {
+  // exhausted run: fold the (allreduced) final pass into the totals so counts = bincount(L_T)
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  CK(cudaMemcpyAsync(e->st_host, e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  e->st_host->done = 0;
+  e->st_host->need_host = 0;
+  e->st_host->exhausted = 1;
+  CK(cudaMemcpyAsync(e->st, e->st_host, sizeof(DevState), cudaMemcpyHostToDevice, e->stream));
+  if ((r = launch_finish(e, 0, !e->last_pass_full))) return r;
+  CK(cudaStreamSynchronize(e->stream));
   return KM_OK;
 }
 
@@ -1072,8 +1125,9 @@ int km_step_repair_apply(km_engine* e, int32_t empty_cluster, int32_t owner_is_m
   cudaSetDevice(e->device);
   double* dc = e->scratch_d;
   CK(cudaMemcpyAsync(dc, coords, 8 * (size_t)e->m, cudaMemcpyHostToDevice, e->stream));
-  repair_apply_global_kernel<<<1, 32, 0, e->stream>>>(empty_cluster, owner_is_me, local_row, dc, donor, e->m,
-                                                             e->labels, e->d2, e->model_counts, e->cur);
+  repair_apply_global_kernel<<<1, 32, 0, e->stream>>>(empty_cluster, owner_is_me, local_row, dc, donor, e->k,
+                                                      e->m, e->labels, e->d2, e->model_counts, e->cur, e->tot,
+                                                      std::ldexp(1.0, e->frac_bits));
   CK_LAUNCH("repair_apply_global_kernel");
   CK(cudaStreamSynchronize(e->stream));
   e->stats.repairs += 1;

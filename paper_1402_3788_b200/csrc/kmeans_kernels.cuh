@@ -22,6 +22,7 @@
 //    blocks, model.py:18-24; we get it from exact integer arithmetic).
 #pragma once
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 #include "kmeans_state.h"
@@ -241,11 +242,20 @@ __global__ void __launch_bounds__(kThreads) lloyd_pass_kernel(PassArgs a) {
         if (lab < 0 || lab >= k) { bad = 1; lab = -1; }
       }
       if (lab >= 0) {
-        atomicAdd(cnt + lab, 1ull);
-        if (DO_SUMS) {
-          unsigned long long* dst = acc + (size_t)lab * m;
-          for (int f = 0; f < m; ++f)
-            atomicAdd(dst + f, (unsigned long long)to_fixed<T>(xrow[f], a.scale_f, a.scale_d, a.use_dscale));
+        if (SMEM_ACC) {
+          atomicAdd(reinterpret_cast<unsigned int*>(cnt + lab), 1u);  // counts < 2^32 per CTA
+          if (DO_SUMS) {
+            unsigned long long* dst = acc + (size_t)lab * m;
+            for (int f = 0; f < m; ++f)
+              smem_add64(dst + f, (unsigned long long)to_fixed<T>(xrow[f], a.scale_f, a.scale_d, a.use_dscale));
+          }
+        } else {
+          atomicAdd(cnt + lab, 1ull);
+          if (DO_SUMS) {
+            unsigned long long* dst = acc + (size_t)lab * m;
+            for (int f = 0; f < m; ++f)
+              atomicAdd(dst + f, (unsigned long long)to_fixed<T>(xrow[f], a.scale_f, a.scale_d, a.use_dscale));
+          }
         }
       }
     }
@@ -273,15 +283,18 @@ __global__ void __launch_bounds__(kThreads) lloyd_pass_kernel(PassArgs a) {
 // (engine.converged, engine.py:297-310) and the fp32 filter prep.
 // ---------------------------------------------------------------------------
 struct FinishArgs {
-  unsigned long long* part;  // k·m sums + k counts (zeroed after use unless the loop ends)
+  unsigned long long* part;  // k·m sums + k counts of the last pass (Δ or full; zeroed once consumed)
+  unsigned long long* tot;   // k·m sums + k counts of the current labels (running totals)
+  int32_t accumulate;        // 1: tot += part (incremental pass), 0: tot = part (full pass)
   double* cur;               // k × m current centres (in: C_{t-1}; out: C_t)
   double* prev;              // k × m (out: C_{t-1})
   long long* model_counts;   // k (out)
   float* w;                  // k × mpad (out: −2·fl32(C_t))
   float* cn;                 // k
   float* cmax;               // [0]
-  float* wsplit;             // [2][kp][32] tensor-core filter operand (nullable)
+  unsigned short* wop;       // [2kp][64] fp16 tensor-core B operand (nullable): [wh|wh], [wl|0]
   int32_t kp;
+  float pre;                 // power-of-two prescale of the tensor-core operands
   int32_t k, m, mpad;
   double inv_scale;          // 2^-F
   DevState* st;
@@ -289,31 +302,39 @@ struct FinishArgs {
 };
 
 __device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, float* w, float* cn, float* cmax,
-                                                  int k, int m, int mpad, float* s_red, float* wsplit = nullptr,
-                                                  int kp = 0) {
-  // tensor-core operand W~ (hi/lo tf32 split): rows c < k = (−2·fl32(c_f), f < m; ‖fl32(c)‖² at f = m)
-  if (wsplit != nullptr) {
+                                                  int k, int m, int mpad, float* s_red,
+                                                  unsigned short* wop = nullptr, int kp = 0, float pre = 1.f) {
+  // tensor-core B operand (fp16 hi/lo split of W~' = 2^s·(−2·fl32(c)), 2^2s·‖fl32(c)‖² at f = m):
+  // row c < kp: [wh_c | wh_c], row kp + c: [wl_c | 0]  (64 halfs = one 128-byte SW128 row)
+  if (wop != nullptr) {
+    const int hw = 8 * ((m + 1 + 7) / 8);  // halfs per part (features incl. the ‖c‖² column)
+    for (int i = threadIdx.x; i < kp * 64; i += blockDim.x) wop[i + kp * 64] = 0, wop[i] = 0;
+    __syncthreads();
     for (int i = threadIdx.x; i < kp * 32; i += blockDim.x) {
       const int cc = i >> 5, f = i & 31;
       float v = 0.f;
       if (cc < k) {
         if (f < m) {
-          v = -2.0f * __double2float_rn(c[(size_t)cc * m + f]);
+          v = -2.0f * __double2float_rn(c[(size_t)cc * m + f]) * pre;
         } else if (f == m) {
           double s = 0.0;
           for (int g = 0; g < m; ++g) {
             const double e = (double)__double2float_rn(c[(size_t)cc * m + g]);
             s = __fma_rn(e, e, s);
           }
-          v = __double2float_rn(s);
+          v = __double2float_rn(s * (double)pre * (double)pre);
         }
       }
-      const float h = __uint_as_float(__float_as_uint(v) & 0xffffe000u);
-      wsplit[i] = h;
-      wsplit[kp * 32 + i] = v - h;
+      const __half h = __float2half_rn(v);
+      const __half l = __float2half_rn(v - __half2float(h));
+      const unsigned short hb = __half_as_ushort(h), lb = __half_as_ushort(l);
+      if (f < hw) {
+        wop[(size_t)cc * 64 + f] = hb;
+        wop[(size_t)cc * 64 + hw + f] = hb;
+        wop[(size_t)(kp + cc) * 64 + f] = lb;
+      }
     }
   }
-  // w = −2·fl32(c) (exact scaling), cn = fl32(Σ fl32(c)²), cmax = max √(Σ fl32(c)²) rounded up.
   for (int i = threadIdx.x; i < k * mpad; i += blockDim.x) {
     const int cc = i / mpad, f = i - cc * mpad;
     w[i] = (f < m) ? -2.0f * __double2float_rn(c[(size_t)cc * m + f]) : 0.0f;
@@ -365,7 +386,7 @@ __device__ __forceinline__ int block_converged(const double* __restrict__ prev, 
 __device__ __forceinline__ void loop_check(FinishArgs& a, double* s_redd, float* s_red) {
   DevState* st = a.st;
   const int conv = block_converged(a.prev, a.cur, a.k, a.m, st->tol, s_redd);
-  block_prep_filter(a.cur, a.w, a.cn, a.cmax, a.k, a.m, a.mpad, s_red, a.wsplit, a.kp);
+  block_prep_filter(a.cur, a.w, a.cn, a.cmax, a.k, a.m, a.mpad, s_red, a.wop, a.kp, a.pre);
   if (threadIdx.x == 0) {
     st->need_host = 0;
     if (conv) {
@@ -382,17 +403,29 @@ __global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a) {
   __shared__ double s_redd[32];
   __shared__ int s_empty[32];
   DevState* st = a.st;
+  const int k = a.k, m = a.m;
   if (a.mode == 0) {
     if (st->done || st->need_host) return;
-    if (st->exhausted) {  // the final assign pass has run: L_T and bincount(L_T) are in place
+    if (st->exhausted) {  // the final assign pass has run: fold its Δ so tot counts = bincount(L_T)
+      for (int i = threadIdx.x; i < k * m + k; i += blockDim.x) {
+        a.tot[i] = a.accumulate ? a.tot[i] + a.part[i] : a.part[i];
+        a.part[i] = 0ull;
+      }
+      __syncthreads();
+      for (int cc = threadIdx.x; cc < k; cc += blockDim.x) a.model_counts[cc] = (long long)a.tot[(size_t)k * m + cc];
       if (threadIdx.x == 0) st->done = 1;
       return;
     }
   }
-  const int k = a.k, m = a.m;
-  unsigned long long* sums = a.part;
-  unsigned long long* cnts = a.part + (size_t)k * m;
-  // prev ← cur ; cur ← S/N
+  // running totals of the current labels (exact integer arithmetic: Δ-updates == recomputation)
+  for (int i = threadIdx.x; i < k * m + k; i += blockDim.x) {
+    a.tot[i] = a.accumulate ? a.tot[i] + a.part[i] : a.part[i];
+    a.part[i] = 0ull;
+  }
+  __syncthreads();
+  unsigned long long* sums = a.tot;
+  unsigned long long* cnts = a.tot + (size_t)k * m;
+  // prev ← cur ; cur ← S/N  (engine._finish_update, engine.py:249-263)
   for (int i = threadIdx.x; i < k * m; i += blockDim.x) {
     const int cc = i / m;
     const long long nc = (long long)cnts[cc];
@@ -415,8 +448,6 @@ __global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a) {
   __syncthreads();
   int total_empty = 0;
   for (int i = 0; i < (int)(blockDim.x >> 5); ++i) total_empty += s_empty[i];
-  // consumed: zero the accumulators for the next pass
-  for (int i = threadIdx.x; i < k * m + k; i += blockDim.x) a.part[i] = 0ull;
   if (a.mode == 1) {
     if (threadIdx.x == 0) st->n_empty = total_empty;
     return;
@@ -442,9 +473,10 @@ __global__ void __launch_bounds__(512) lloyd_check_kernel(FinishArgs a) {
 
 // Filter prep only (initial centres, standalone assign).
 __global__ void __launch_bounds__(512) prep_filter_kernel(const double* c, float* w, float* cn, float* cmax,
-                                                          int k, int m, int mpad, float* wsplit, int kp) {
+                                                          int k, int m, int mpad, unsigned short* wop, int kp,
+                                                          float pre) {
   __shared__ float s_red[32];
-  block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red, wsplit, kp);
+  block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red, wop, kp, pre);
 }
 
 // Standalone congruence test (km_converged).
@@ -493,10 +525,22 @@ __global__ void argmax_partial_kernel(const double* __restrict__ d2, int64_t n, 
 }
 
 // One thread: reduce the partials, apply the relabel for empty cluster `c`.
+// Move sample s (fixed-point coordinates) from cluster `donor` to `c` in the running totals.
+__device__ __forceinline__ void move_in_totals(unsigned long long* tot, int k, int m, int donor, int c,
+                                               const double* coords, double scale_d) {
+  for (int f = 0; f < m; ++f) {
+    const unsigned long long v = (unsigned long long)__double2ll_rn(__dmul_rn(coords[f], scale_d));
+    tot[(size_t)donor * m + f] -= v;
+    tot[(size_t)c * m + f] += v;
+  }
+  tot[(size_t)k * m + donor] -= 1ull;
+  tot[(size_t)k * m + c] += 1ull;
+}
+
 template <typename T>
-__global__ void repair_apply_kernel(const ArgMax* partial, int nparts, int c, const T* __restrict__ x, int m,
+__global__ void repair_apply_kernel(const ArgMax* partial, int nparts, int c, const T* __restrict__ x, int k, int m,
                                     int32_t* labels, double* d2, long long* model_counts, double* cur,
-                                    ArgMax* winner_out) {
+                                    unsigned long long* tot, double scale_d, ArgMax* winner_out) {
   if (threadIdx.x != 0) return;
   ArgMax best = partial[0];
   for (int i = 1; i < nparts; ++i) best = argmax_better(best, partial[i]);
@@ -506,6 +550,7 @@ __global__ void repair_apply_kernel(const ArgMax* partial, int nparts, int c, co
   model_counts[donor] -= 1;
   model_counts[c] += 1;
   for (int f = 0; f < m; ++f) cur[(size_t)c * m + f] = to_f64(x[s * m + f]);
+  move_in_totals(tot, k, m, donor, c, cur + (size_t)c * m, scale_d);
   d2[s] = 0.0;
   if (winner_out) *winner_out = best;
 }
@@ -520,8 +565,8 @@ __global__ void argmax_final_kernel(const ArgMax* partial, int nparts, ArgMax* o
 
 // Apply a repair decided across shards.
 __global__ void repair_apply_global_kernel(int c, int owner, long long local_row, const double* coords, int donor,
-                                           int m, int32_t* labels, double* d2, long long* model_counts,
-                                           double* cur) {
+                                           int k, int m, int32_t* labels, double* d2, long long* model_counts,
+                                           double* cur, unsigned long long* tot, double scale_d) {
   if (threadIdx.x != 0) return;
   if (owner) {
     labels[local_row] = c;
@@ -530,6 +575,7 @@ __global__ void repair_apply_global_kernel(int c, int owner, long long local_row
   model_counts[donor] -= 1;
   model_counts[c] += 1;
   for (int f = 0; f < m; ++f) cur[(size_t)c * m + f] = coords[f];
+  move_in_totals(tot, k, m, donor, c, coords, scale_d);
 }
 
 // ---------------------------------------------------------------------------

@@ -15,7 +15,21 @@ struct DevState {
   int32_t max_iters;
   int32_t bad_label;  // first invalid label seen by a sums-only pass (+1), 0 = none
   unsigned long long rechecked;
+  unsigned long long changed;   // labels that changed in incremental passes
   double tol;
 };
+
+#ifdef __CUDACC__
+// Exact 64-bit (mod 2^64) add into shared memory with two native 32-bit atomics
+// (a 64-bit shared atomicAdd compiles to a CAS spin loop on sm_100a).
+__device__ __forceinline__ void smem_add64(unsigned long long* addr, unsigned long long v) {
+  unsigned int* p = reinterpret_cast<unsigned int*>(addr);
+  const unsigned int lo = (unsigned int)v, hi = (unsigned int)(v >> 32);
+  const unsigned int old = atomicAdd(p, lo);
+  const unsigned int h = hi + ((old + lo) < old ? 1u : 0u);
+  if (h) atomicAdd(p + 1, h);
+}
+
+#endif
 
 }  // namespace km

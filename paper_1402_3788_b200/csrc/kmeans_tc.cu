@@ -41,6 +41,8 @@ static int launch_kp(const TcArgs& a, int kp, int num_sms, size_t smem_optin, cu
     case 32: return launch_t<MP, 32>(a, num_sms, smem_optin, stream, ce, msg, len);
     case 48: return launch_t<MP, 48>(a, num_sms, smem_optin, stream, ce, msg, len);
     case 64: return launch_t<MP, 64>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 96: return launch_t<MP, 96>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 128: return launch_t<MP, 128>(a, num_sms, smem_optin, stream, ce, msg, len);
     default: snprintf(msg, len, "tensor-core pass: unsupported k padding %d", kp); return 2;
   }
 }

@@ -15,23 +15,24 @@ struct TcArgs {
   const float* x;          // n × m fp32 row-major
   int64_t n;
   int32_t m, k;
-  const float* wsplit;     // [2][KP][32] : tf32 hi, lo of W~ rows (prepared by the finish kernel)
-  const float* cmax;       // [0] max ‖fl32(c)‖ rounded up
+  const unsigned short* wop;  // [2KP][64] fp16 B operand rows ([wh|wh], [wl|0]) from the prep/finish kernel
+  const float* cmax;       // [0] max ‖fl32(c)‖ (unscaled, rounded up)
   const double* c64;       // k × m fp64 centres (exact recheck)
-  int32_t* labels;
-  unsigned long long* part;  // k·m sums + k counts (int64 fixed point)
-  float scale_f;           // 2^F
+  int32_t* labels;         // in: L_{t-1} (incremental) / out: L_t (written where changed)
+  unsigned long long* part;  // Δ (incremental) or full per-cluster fixed-point sums + counts
+  float pre;               // 2^s operand prescale (|x·pre| < 1)
+  float scale_f;           // 2^F fixed point
   double scale_d;
   int32_t use_dscale;
   float err_coef;          // certified bound coefficient for the tensor-core scores
-  float err_floor;
+  float err_floor;         // absolute floor (prescaled units)
   float nx_inflate;
   int32_t exact_only;
+  int32_t full;            // 1: old labels invalid (first pass / standalone assign): add every point
   DevState* st;
   int32_t gate;
-  int32_t do_sums;         // 0: assign only (counts still accumulated)
-  float* dbg_scores;       // optional n × k raw tensor-core scores (tests)
-  int32_t dbg_flags;       // tuning experiments only: 1 = skip update MMAs, 2 = skip assign MMAs
+  float* dbg_scores;       // optional n × k raw tensor-core scores, unscaled (tests)
+  int32_t dbg_flags;       // tuning experiments only: 2 = skip assign MMAs
   long long* dbg_times;    // tuning experiments only: per-tile clock64 stamps of CTA 0
 };
 

@@ -143,11 +143,10 @@ def run_sharded(engine, coll, c0, max_iters=1000, tol=0.0, want_labels=True) -> 
         if t >= max_iters:
             engine.step_pass()               # L_T = A(C_T); counts = global bincount(L_T)
             coll.allreduce_sum_(part)
+            engine.step_fold()
             break
         engine.step_pass()
     centers, counts, labels = engine.step_read(k, want_labels=want_labels)
-    if not converged:
-        counts = part[k * engine.m:].cpu().numpy().astype(np.int64).copy()
     return ShardResult(centers, counts, labels, t, converged, row_offset)
 
 
