@@ -67,8 +67,12 @@ struct km_engine {
   unsigned short* wop = nullptr;    // [2kp][64] fp16 tensor-core B operand ([wh|wh], [wl|0])
   int32_t kp = 0;                   // k padded for the tensor-core N dimension (16..128)
   float pre = 1.f;                  // power-of-two prescale of the tensor-core operands
+  float xnorm_max = 0.f;            // max ‖x_i‖ over the resident points (rounded up)
+  bool prescale = true;             // multiply x by `pre` in the tensor-core pass
   unsigned long long* tot = nullptr;  // running per-cluster totals (k·m sums + k counts)
   bool next_full = true;            // next TC pass must add every point (no valid previous labels)
+  long long* recheck_rows = nullptr;     // queue of uncertified points (n)
+  unsigned int* recheck_count = nullptr;
   bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
   int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required
   float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
@@ -208,6 +212,7 @@ static int launch_tc(km_engine* e, bool full, bool gated) {
   a.k = e->k;
   a.wop = e->wop;
   a.cmax = e->cmax;
+  a.xnorm_max = e->xnorm_max;
   a.c64 = e->cur;
   a.labels = e->labels;
   a.part = e->part;
@@ -218,10 +223,15 @@ static int launch_tc(km_engine* e, bool full, bool gated) {
   a.scale_f = a.use_dscale ? 1.0f : (float)std::ldexp(1.0, F);
   const int mp = tc_mp_for(e->m);
   a.err_coef = host_err_coef_tc(e->m, mp);
-  a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -22));
+  // absolute floor (operand units): fp16 subnormal spacing 2^-24 per element times |w| ≤ 2·max‖x‖·pre
+  a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -23) * (1.0 + 2.0 * e->xnorm_max * e->pre));
   a.nx_inflate = (float)(1.0 + (e->m + 2) * std::ldexp(1.0, -24));
   a.exact_only = (e->absmax > std::ldexp(1.0, 50)) ? 1 : 0;
   a.full = full ? 1 : 0;
+  a.exact_m = 1;
+  a.prescale = e->prescale ? 1 : 0;
+  a.recheck_rows = e->recheck_rows;
+  a.recheck_count = e->recheck_count;
   a.st = e->st;
   a.gate = gated ? 1 : 0;
   a.dbg_scores = e->dbg_scores;
@@ -238,7 +248,9 @@ static int launch_tc(km_engine* e, bool full, bool gated) {
   const int rc = tc::launch(a, mp, e->kp, e->num_sms, e->smem_optin, e->stream, &c, msg, sizeof msg);
   if (rc == 1) return cuda_fail(e, c, msg);
   if (rc == 2) return set_err(e, KM_ERR_CAPACITY, "%s", msg);
-  e->stats.kernel_launches += 1;
+  c = tc::launch_recheck(a, e->num_sms, e->stream);
+  if (c != cudaSuccess) return cuda_fail(e, c, "recheck_kernel launch");
+  e->stats.kernel_launches += 2;
   if (a.dbg_times) {
     long long h[64 * 8];
     cudaMemcpyAsync(h, a.dbg_times, sizeof h, cudaMemcpyDeviceToHost, e->stream);
@@ -247,9 +259,9 @@ static int launch_tc(km_engine* e, bool full, bool gated) {
     if (f) {
       for (int i = 0; i < 64; ++i) {
         if (!h[i * 8]) continue;
-        fprintf(f, "tile %2d", i);
-        for (int q = 1; q < 7; ++q) fprintf(f, " %6lld", h[i * 8 + q] - h[i * 8 + q - 1]);
-        fprintf(f, "  | start %lld\n", h[i * 8] - h[0]);
+        const long long* t = h + i * 8;  // transform: raw wait, compute, A-buffer wait, store; epilogue: s wait, body
+        fprintf(f, "tile %2d  T: raw %5lld comp %5lld awaitA %5lld sts %5lld | E: swait %5lld body %5lld | t0 %lld\n", i,
+                t[1] - t[0], t[7] - t[1], t[2] - t[7], t[3] - t[2], t[5] - t[4], t[6] - t[5], t[0] - h[0]);
       }
       fprintf(f, "----\n");
       fclose(f);
@@ -323,6 +335,7 @@ static FinishArgs finish_args(km_engine* e, int mode, bool accumulate) {
   f.part = e->part;
   f.tot = e->tot;
   f.accumulate = accumulate ? 1 : 0;
+  f.recheck_count = e->recheck_count;
   f.cur = e->cur;
   f.prev = e->prev;
   f.model_counts = e->model_counts;
@@ -400,10 +413,12 @@ static int grid_for(km_engine* e, int64_t n, int per_sm = 8) {
 static void free_k(km_engine* e) {
   dfree(e->labels); dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
   dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->d2); dfree(e->partials); dfree(e->winner);
-  dfree(e->scratch_d); dfree(e->labels64); dfree(e->wop); dfree(e->tot);
+  dfree(e->scratch_d); dfree(e->labels64); dfree(e->wop); dfree(e->tot); dfree(e->recheck_rows);
+  dfree(e->recheck_count);
   e->labels = nullptr; e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
   e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->d2 = nullptr; e->partials = nullptr; e->winner = nullptr;
   e->scratch_d = nullptr; e->labels64 = nullptr; e->wop = nullptr; e->tot = nullptr;
+  e->recheck_rows = nullptr; e->recheck_count = nullptr;
   e->k = 0;
   e->kp = 0;
 }
@@ -432,6 +447,9 @@ static int ensure_k(km_engine* e, int32_t k) {
   if ((r = dalloc(e, &e->wop, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp))) return r;
   CK(cudaMemsetAsync(e->wop, 0, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp, e->stream));
   if ((r = dalloc(e, &e->tot, 8 * ((size_t)k * m + k)))) return r;
+  if ((r = dalloc(e, &e->recheck_rows, 8 * (size_t)e->n))) return r;
+  if ((r = dalloc(e, &e->recheck_count, 16))) return r;
+  CK(cudaMemsetAsync(e->recheck_count, 0, 16, e->stream));
   CK(cudaMemsetAsync(e->tot, 0, 8 * ((size_t)k * m + k), e->stream));
   e->next_full = true;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * m + k), e->stream));
@@ -475,10 +493,29 @@ static int scan_points(km_engine* e, const void* x, int bytes_per, int64_t count
 }
 
 static int after_points_loaded(km_engine* e) {
+  {  // max ‖x_i‖ for the tensor-core filter bound
+    unsigned int zero = 0, bits = 0;
+    CK(cudaMemcpyAsync(e->scratch_u, &zero, 4, cudaMemcpyHostToDevice, e->stream));
+    const int g = grid_for(e, e->n, 4);
+    if (e->point_bytes == 4)
+      rownorm_max_kernel<float><<<g, 256, 0, e->stream>>>((const float*)e->x, e->n, e->m, (unsigned int*)e->scratch_u);
+    else
+      rownorm_max_kernel<double><<<g, 256, 0, e->stream>>>((const double*)e->x, e->n, e->m, (unsigned int*)e->scratch_u);
+    CK_LAUNCH("rownorm_max_kernel");
+    e->stats.kernel_launches += 1;
+    CK(cudaMemcpyAsync(&bits, e->scratch_u, 4, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    std::memcpy(&e->xnorm_max, &bits, 4);
+  }
   if (!e->frac_user) e->frac_bits = compute_frac_bits(e->absmax, e->n);
-  // tensor-core operand prescale 2^s: |x·2^s| < 1 (exact power of two)
+  // tensor-core operands are fp16: data already in a safe range (|x| ≥ 2^-4 scale, every score
+  // |S| ≤ 4·m·max|x|² ≤ 2^15 < the +65504 padding score) go as is; otherwise prescale by an exact
+  // power of two 2^s with |x·2^s| < 1
   e->pre = 1.f;
-  if (e->absmax > 0.0 && e->absmax < std::ldexp(1.0, 100)) {
+  e->prescale = true;
+  if (e->absmax >= std::ldexp(1.0, -4) && 4.0 * e->m * e->absmax * e->absmax <= 32768.0) {
+    e->prescale = false;
+  } else if (e->absmax > 0.0 && e->absmax < std::ldexp(1.0, 100)) {
     const int s = -(std::ilogb(e->absmax) + 1);
     e->pre = (float)std::ldexp(1.0, std::max(-120, std::min(120, s)));
   }
@@ -758,6 +795,7 @@ int km_assign(km_engine* e, const double* centers, int32_t k, int64_t* labels_ou
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   if ((r = launch_pass(e, PASS_ASSIGN_ONLY, false))) return r;
   e->stats.passes += 1;
+  CK(cudaMemsetAsync(e->recheck_count, 0, 4, e->stream));
   if (labels_out && (r = download_labels(e, labels_out))) return r;
   if (counts_out)
     CK(cudaMemcpyAsync(counts_out, e->part + (size_t)k * e->m, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
@@ -1202,6 +1240,7 @@ int km_debug_filter_scores(km_engine* e, const double* centers, int32_t k, float
   e->dbg_scores = dbg;
   r = launch_pass(e, PASS_ASSIGN_ONLY, false);
   e->dbg_scores = nullptr;
+  cudaMemsetAsync(e->recheck_count, 0, 4, e->stream);
   cudaError_t c = cudaSuccess;
   if (!r) c = cudaMemcpyAsync(out, dbg, sizeof(float) * (size_t)e->n * k, cudaMemcpyDeviceToHost, e->stream);
   if (!r && c == cudaSuccess) c = cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream);

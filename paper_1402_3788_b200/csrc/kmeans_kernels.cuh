@@ -286,6 +286,7 @@ struct FinishArgs {
   unsigned long long* part;  // k·m sums + k counts of the last pass (Δ or full; zeroed once consumed)
   unsigned long long* tot;   // k·m sums + k counts of the current labels (running totals)
   int32_t accumulate;        // 1: tot += part (incremental pass), 0: tot = part (full pass)
+  unsigned int* recheck_count;  // deferred-recheck queue length of the last pass (reset here)
   double* cur;               // k × m current centres (in: C_{t-1}; out: C_t)
   double* prev;              // k × m (out: C_{t-1})
   long long* model_counts;   // k (out)
@@ -304,41 +305,11 @@ struct FinishArgs {
 __device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, float* w, float* cn, float* cmax,
                                                   int k, int m, int mpad, float* s_red,
                                                   unsigned short* wop = nullptr, int kp = 0, float pre = 1.f) {
-  // tensor-core B operand (fp16 hi/lo split of W~' = 2^s·(−2·fl32(c)), 2^2s·‖fl32(c)‖² at f = m):
-  // row c < kp: [wh_c | wh_c], row kp + c: [wl_c | 0]  (64 halfs = one 128-byte SW128 row)
-  if (wop != nullptr) {
-    const int hw = 8 * ((m + 1 + 7) / 8);  // halfs per part (features incl. the ‖c‖² column)
-    for (int i = threadIdx.x; i < kp * 64; i += blockDim.x) wop[i + kp * 64] = 0, wop[i] = 0;
-    __syncthreads();
-    for (int i = threadIdx.x; i < kp * 32; i += blockDim.x) {
-      const int cc = i >> 5, f = i & 31;
-      float v = 0.f;
-      if (cc < k) {
-        if (f < m) {
-          v = -2.0f * __double2float_rn(c[(size_t)cc * m + f]) * pre;
-        } else if (f == m) {
-          double s = 0.0;
-          for (int g = 0; g < m; ++g) {
-            const double e = (double)__double2float_rn(c[(size_t)cc * m + g]);
-            s = __fma_rn(e, e, s);
-          }
-          v = __double2float_rn(s * (double)pre * (double)pre);
-        }
-      }
-      const __half h = __float2half_rn(v);
-      const __half l = __float2half_rn(v - __half2float(h));
-      const unsigned short hb = __half_as_ushort(h), lb = __half_as_ushort(l);
-      if (f < hw) {
-        wop[(size_t)cc * 64 + f] = hb;
-        wop[(size_t)cc * 64 + hw + f] = hb;
-        wop[(size_t)(kp + cc) * 64 + f] = lb;
-      }
-    }
-  }
-  for (int i = threadIdx.x; i < k * mpad; i += blockDim.x) {
-    const int cc = i / mpad, f = i - cc * mpad;
-    w[i] = (f < m) ? -2.0f * __double2float_rn(c[(size_t)cc * m + f]) : 0.0f;
-  }
+  // per centre: ‖fl32(c)‖² (fp64 sum of the fp32-rounded coordinates, rounded to fp32), its root
+  // rounded up for the filter bound; then the SIMT operand w = −2·fl32(c) (zero padded) and the
+  // tensor-core operand (fp16 hi/lo split of W~' = 2^s·(−2·fl32(c)), 2^2s·‖fl32(c)‖² at f = m):
+  // row c < kp: [wh_c | wh_c], row kp + c: [wl_c | 0]  (hw halfs per part, 64-half rows)
+  __shared__ double s_cn2[1024];
   float local_max = 0.f;
   for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
     double s = 0.0;
@@ -346,11 +317,14 @@ __device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, 
       const double v = (double)__double2float_rn(c[(size_t)cc * m + f]);
       s = __fma_rn(v, v, s);
     }
+    if (cc < 1024) s_cn2[cc] = s;
     cn[cc] = __double2float_rn(s);
-    const float r = __double2float_ru(sqrt(s) * (1.0 + 1e-12));
-    local_max = fmaxf(local_max, r);
+    local_max = fmaxf(local_max, __double2float_ru(sqrt(s) * (1.0 + 1e-12)));
   }
-  // block max
+  for (int i = threadIdx.x; i < k * mpad; i += blockDim.x) {
+    const int cc = i / mpad, f = i - cc * mpad;
+    w[i] = (f < m) ? -2.0f * __double2float_rn(c[(size_t)cc * m + f]) : 0.0f;
+  }
   for (int o = 16; o > 0; o >>= 1) local_max = fmaxf(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local_max;
   __syncthreads();
@@ -358,6 +332,24 @@ __device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, 
     float mx = 0.f;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_red[i]);
     cmax[0] = mx;
+  }
+  if (wop != nullptr) {
+    const int hw = 8 * ((m + 1 + 7) / 8);
+    for (int i = threadIdx.x; i < kp * 64; i += blockDim.x) {
+      const int cc = i >> 6, col = i & 63;
+      const int f = col < hw ? col : col - hw;  // feature of this column (part 0 or 1)
+      float v = 0.f;
+      if (cc < k && col < 2 * hw) {
+        if (f < m) v = -2.0f * __double2float_rn(c[(size_t)cc * m + f]) * pre;
+        else if (f == m) v = __double2float_rn(s_cn2[cc] * (double)pre * (double)pre);
+      } else if (cc >= k && col < 2 * hw && f == m) {
+        v = 65504.f;  // padded centre: score +65504 (fp16 max) > every real score, never selected
+      }
+      const __half h = __float2half_rn(v);
+      const __half l = __float2half_rn(v - __half2float(h));
+      wop[i] = (col < 2 * hw) ? __half_as_ushort(h) : (unsigned short)0;                  // [wh | wh]
+      wop[kp * 64 + i] = (col < hw) ? __half_as_ushort(l) : (unsigned short)0;             // [wl | 0 ]
+    }
   }
   __syncthreads();
 }
@@ -406,6 +398,10 @@ __global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a) {
   const int k = a.k, m = a.m;
   if (a.mode == 0) {
     if (st->done || st->need_host) return;
+    if (threadIdx.x == 0 && a.recheck_count) {  // the recheck kernel of this pass has completed
+      st->rechecked += *a.recheck_count;
+      *a.recheck_count = 0u;
+    }
     if (st->exhausted) {  // the final assign pass has run: fold its Δ so tot counts = bincount(L_T)
       for (int i = threadIdx.x; i < k * m + k; i += blockDim.x) {
         a.tot[i] = a.accumulate ? a.tot[i] + a.part[i] : a.part[i];
@@ -630,6 +626,22 @@ __global__ void absmax_kernel(const T* __restrict__ x, int64_t count, unsigned l
     if (bad) atomicOr(flags, 1);
     if (inexact) atomicOr(flags + 1, 1);
   }
+}
+
+// max over rows of ‖x_i‖ (fp64 sums, rounded up to fp32) for the per-launch filter bound
+template <typename T>
+__global__ void rownorm_max_kernel(const T* __restrict__ x, int64_t n, int m, unsigned int* out_bits) {
+  float mx = 0.f;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int f = 0; f < m; ++f) {
+      const double v = to_f64(x[i * m + f]);
+      s = __fma_rn(v, v, s);
+    }
+    mx = fmaxf(mx, __double2float_ru(sqrt(s) * (1.0 + 1e-12)));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out_bits, __float_as_uint(mx));  // non-negative floats order as uints
 }
 
 __global__ void narrow_f64_kernel(const double* __restrict__ in, int64_t count, float* __restrict__ out) {

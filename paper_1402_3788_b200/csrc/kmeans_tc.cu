@@ -3,59 +3,91 @@
 #include <cstdio>
 
 #include "kmeans_tc.cuh"
+#include "kmeans_tc_dispatch.h"
 
 namespace km {
 namespace tc {
 
-template <int MP, int KP>
-static int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_t stream, cudaError_t* ce,
-                    char* msg, size_t len) {
-  auto kern = lloyd_pass_tc_kernel<MP, KP>;
-  const size_t smem = TcSmem<MP, KP>(a.m).total;
-  if (smem > smem_optin) {
-    snprintf(msg, len, "tensor-core pass needs %zu B of shared memory (max %zu)", smem, smem_optin);
-    return 2;
+// Exact re-decision of the queued points: the reference's fp64 recurrence over
+// ALL centres (_kernels.py:22-45: features ascending, no FMA; argmin with the
+// lowest index on ties), then the same Δ update of the fixed-point sums
+// (global atomics).  One warp per queued point, lane = centre (each lane keeps
+// the reference's sequential feature order); centres staged in shared memory.
+__global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ x, int m, int k,
+                                                      const double* __restrict__ c64, int32_t* labels,
+                                                      const long long* rows, const unsigned int* count,
+                                                      unsigned long long* part, float scale_f, double scale_d,
+                                                      int use_dscale, int full, DevState* st, int gate) {
+  if (gate && (st->done || st->need_host)) return;
+  const unsigned int cnt = *count;
+  if (cnt == 0) return;
+  extern __shared__ double s_c[];  // k × m when it fits (host decides), else global
+  const bool staged = k * m <= 6144;
+  if (staged) {
+    for (int i = threadIdx.x; i < k * m; i += blockDim.x) s_c[i] = c64[i];
+    __syncthreads();
   }
-  cudaError_t c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc smem)"); return 1; }
-  c = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc carveout)"); return 1; }
-  int per_sm = 0;
-  c = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsTC, smem);
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "occupancy(tc)"); return 1; }
-  if (per_sm < 1) { snprintf(msg, len, "tensor-core pass does not fit on an SM"); return 2; }
-  per_sm = std::min(per_sm, 1);  // one persistent CTA per SM (two ping-pong warpgroups inside)
-  const int64_t ntiles = (a.n + kTile - 1) / kTile;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * num_sms));
-  kern<<<(unsigned)grid, kThreadsTC, smem, stream>>>(a);
-  c = cudaGetLastError();
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "lloyd_pass_tc_kernel launch"); return 1; }
-  return 0;
+  const double* C = staged ? s_c : c64;
+  const int lane = threadIdx.x & 31;
+  const unsigned int warps = (gridDim.x * blockDim.x) >> 5;
+  for (unsigned int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < cnt; q += warps) {
+    const long long row = rows[q];
+    const float* xr = x + row * m;
+    const float xl = lane < m ? __ldg(xr + lane) : 0.f;  // m ≤ 31 on the tensor-core path
+    double bd = 0.0;
+    int bl = -1;
+    for (int c0 = 0; c0 < k; c0 += 32) {
+      const int c = c0 + lane;
+      double acc = 0.0;
+      for (int f = 0; f < m; ++f) {
+        const double xv = (double)__shfl_sync(0xffffffffu, xl, f);
+        if (c < k) {
+          const double d = __dsub_rn(xv, C[(size_t)c * m + f]);
+          acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+      }
+      if (c < k && (bl < 0 || acc < bd)) { bd = acc; bl = c; }
+    }
+    // warp argmin: smaller distance, then the lower index (the reference's strict '<' scan)
+    for (int o = 16; o > 0; o >>= 1) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
+      if (ol >= 0 && (bl < 0 || od < bd || (od == bd && ol < bl))) { bd = od; bl = ol; }
+    }
+    const int old = full ? -1 : labels[row];
+    if (bl != old) {
+      if (lane == 0) {
+        labels[row] = bl;
+        atomicAdd(part + (size_t)k * m + bl, 1ull);
+        if (old >= 0) atomicAdd(part + (size_t)k * m + old, ~0ull);
+        if (!full) atomicAdd(&st->changed, 1ull);
+      }
+      if (lane < m) {
+        const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xl, scale_d))
+                                       : __float2ll_rn(__fmul_rn(xl, scale_f));
+        atomicAdd(part + (size_t)bl * m + lane, (unsigned long long)v);
+        if (old >= 0) atomicAdd(part + (size_t)old * m + lane, (unsigned long long)(-v));
+      }
+    }
+  }
 }
 
-template <int MP>
-static int launch_kp(const TcArgs& a, int kp, int num_sms, size_t smem_optin, cudaStream_t stream, cudaError_t* ce,
-                     char* msg, size_t len) {
-  switch (kp) {
-    case 16: return launch_t<MP, 16>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 32: return launch_t<MP, 32>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 48: return launch_t<MP, 48>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 64: return launch_t<MP, 64>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 96: return launch_t<MP, 96>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 128: return launch_t<MP, 128>(a, num_sms, smem_optin, stream, ce, msg, len);
-    default: snprintf(msg, len, "tensor-core pass: unsupported k padding %d", kp); return 2;
-  }
+
+cudaError_t launch_recheck(const TcArgs& a, int num_sms, cudaStream_t stream) {
+  const size_t smem = (size_t)a.k * a.m <= 6144 ? (size_t)a.k * a.m * 8 : 0;
+  // one resident warp per queued point (≈ 64 warps/SM): the per-point latency is a few L2 loads
+  recheck_kernel<<<num_sms * 8, 256, smem, stream>>>(a.x, a.m, a.k, a.c64, a.labels, a.recheck_rows, a.recheck_count,
+                                                     a.part, a.scale_f, a.scale_d, a.use_dscale, a.full, a.st, a.gate);
+  return cudaGetLastError();
 }
 
 int launch(const TcArgs& a, int mp, int kp, int num_sms, size_t smem_optin, cudaStream_t stream,
            cudaError_t* ce, char* msg, size_t len) {
-  switch (mp) {
-    case 7: return launch_kp<7>(a, kp, num_sms, smem_optin, stream, ce, msg, len);
-    case 15: return launch_kp<15>(a, kp, num_sms, smem_optin, stream, ce, msg, len);
-    case 23: return launch_kp<23>(a, kp, num_sms, smem_optin, stream, ce, msg, len);
-    case 31: return launch_kp<31>(a, kp, num_sms, smem_optin, stream, ce, msg, len);
-    default: snprintf(msg, len, "tensor-core pass: unsupported feature padding %d", mp); return 2;
+  if (a.exact_m) {
+    const int r = launch_exact(a, a.m, kp, a.prescale != 0, num_sms, smem_optin, stream, ce, msg, len);
+    if (r >= 0) return r;
   }
+  return launch_bucket(a, mp, kp, num_sms, smem_optin, stream, ce, msg, len);
 }
 
 }  // namespace tc

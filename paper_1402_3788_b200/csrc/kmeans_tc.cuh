@@ -19,26 +19,44 @@
 // per CTA); the finish kernel folds Δ into the running totals.  The first
 // pass (no previous labels) adds every point.
 //
-// Warp roles (persistent CTA, one per SM):
-//   warps 0-7 : two compute warpgroups, ping-pong over tiles; thread = point
-//   warp 8    : TMA producer (cp.async.bulk 1-D copies of raw 4·m-byte rows)
-//   warp 9    : TMEM allocator + single-thread MMA issuer
+// Points whose label the filter cannot certify are queued and re-decided by
+// recheck_kernel (the reference's exact fp64 recurrence over all centres), so
+// the rare slow path never stalls the pipelined hot loop.
+//
+// Warp roles (persistent CTA, one per SM), pipelined over 128-point tiles:
+//   warps 0-7  : transform   two groups, alternate tiles: raw tile → fp16 [hi|lo] A operand
+//   warps 8-15 : epilogue    two groups, alternate tiles: TMEM scores → top-2 →
+//                            certify → Δ update (thread = point = TMEM lane)
+//   warp 16    : TMA producer (cp.async.bulk 1-D copies of raw 4·m-byte rows)
+//   warp 17    : TMEM allocator + single-thread MMA issuer
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
 #include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
 
 #include "kmeans_tc.h"
 
 namespace km {
 namespace tc {
 
-constexpr int kGroups = 2;                         // compute warpgroups (ping-pong over tiles)
-constexpr int kComputeWarps = 4 * kGroups;
-constexpr int kProducerWarp = kComputeWarps;       // TMA producer
-constexpr int kMmaWarp = kComputeWarps + 1;        // TMEM allocator + MMA issuer
-constexpr int kThreadsTC = (kComputeWarps + 2) * 32;
-constexpr int kRawStages = 4;
+constexpr int kTransformGroups = 2;                // transform warpgroups (alternate tiles)
+constexpr int kTransformWarps = 4 * kTransformGroups;
+constexpr int kEpiGroups = 2;                      // epilogue warpgroups (alternate tiles)
+constexpr int kEpiWarps = 4 * kEpiGroups;
+constexpr int kProducerWarp = kTransformWarps + kEpiWarps;  // TMA producer
+constexpr int kMmaWarp = kProducerWarp + 1;                 // TMEM allocator + MMA issuer
+constexpr int kThreadsTC = (kMmaWarp + 1) * 32;
+constexpr int kQueueCap = 1024;                    // per-CTA staging of uncertified points (smem)
+// ring depths: raw tiles in flight (TMA → transform) and A operand buffers (transform → MMA);
+// shallower for the widest shapes so the CTA fits in 227 KB of shared memory
+template <int MP, int KP>
+struct TcStages {
+  static constexpr int raw = (MP <= 23 && KP <= 32) ? 6 : 4;
+  static constexpr int a = (MP <= 23 && KP <= 32) ? 6 : 4;
+};
 
 // ---- PTX helpers -----------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -204,25 +222,41 @@ struct TcLayout {
   static constexpr int KSTEPS = (2 * HW) / 16;       // kind::f16 MMA k-steps (16 halfs = 32 B each)
 };
 
+template <int KP>
+struct TcTmem {
+  static constexpr int NS = KP <= 32 ? 8 : KP <= 64 ? 4 : 2;  // TMEM score buffers (2KP columns each)
+  static constexpr uint32_t cols = NS * 2 * KP;
+  static constexpr uint32_t alloc = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
+};
+
 // smem carve-up (1 KiB aligned sections; the raw ring depends on the runtime m)
 template <int MP, int KP>
 struct TcSmem {
-  uint32_t raw_stride, off_raw = 0, off_a, off_w, off_acc, off_bar, total;
+  static constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
+  uint32_t raw_stride, off_raw = 0, off_a, off_w, off_acc, off_q, off_bar, total;
   __host__ __device__ explicit TcSmem(int m) {
-    raw_stride = ((uint32_t)kTile * m * 4 + 1023) & ~1023u;
-    off_a = kRawStages * raw_stride;                 // [kGroups][128 rows × 128 B]
-    off_w = off_a + kGroups * kTile * 128;           // [2KP rows × 128 B]
+    // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
+    raw_stride = ((uint32_t)kTile * m * 4 + 256 + 1023) & ~1023u;
+    off_a = RS * raw_stride;                 // [AS][128 rows × 128 B]
+    off_w = off_a + AS * kTile * 128;          // [2KP rows × 128 B]
     off_acc = off_w + 2 * KP * 128;                  // [KP·(MP+1) + KP] int64 Δ accumulators
-    off_bar = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;
-    total = off_bar + 512 + 1024;                    // barriers + 1 KiB alignment slack
+    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // [kQueueCap] int64 rows + counter
+    off_bar = off_q + kQueueCap * 8 + 1024;
+    total = off_bar + 1024 + 1024;                   // barriers + 1 KiB alignment slack
   }
 };
 
-template <int MP, int KP>
+// MT > 0: exact feature count m = MT (compile-time); MT < 0: runtime m ≤ −MT.
+// PRE: multiply x by the power-of-two prescale (off when the data range is fp16-safe as is).
+template <int MT, int KP, bool PRE>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
+  static_assert(kThreadsTC == 576, "warp-role layout");
+  constexpr int MP = MT > 0 ? MT : -MT;
   if (a.gate && (a.st->done || a.st->need_host)) return;
   using L = TcLayout<MP>;
-  const TcSmem<MP, KP> S(a.m);
+  using TM = TcTmem<KP>;
+  const TcSmem<MP, KP> S(MT > 0 ? MT : a.m);
+  constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1 KiB align the carve-up (SW128 atoms must be 1 KiB aligned); pointer arithmetic on the
   // __shared__ array keeps the shared address space (LDS/STS, not generic LD/ST)
@@ -230,57 +264,67 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   float* raw = reinterpret_cast<float*>(sm + S.off_raw);
   unsigned char* s_w = sm + S.off_w;
   unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(sm + S.off_acc);
+  long long* s_q = reinterpret_cast<long long*>(sm + S.off_q);
+  unsigned int* s_qn = reinterpret_cast<unsigned int*>(sm + S.off_q + kQueueCap * 8);  // [0] count, [1] global base
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S.off_bar);
-  uint64_t* full_raw = bars;                      // [kRawStages]  TMA → compute
-  uint64_t* empty_raw = bars + kRawStages;        // [kRawStages]  compute → TMA
-  uint64_t* op_full = bars + 2 * kRawStages;      // [kGroups] A operand written (compute → MMA)
-  uint64_t* s_full = op_full + kGroups;           // [kGroups] scores in TMEM   (MMA → compute)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_full + kGroups);
+  uint64_t* full_raw = bars;                        // [RS] TMA → transform
+  uint64_t* empty_raw = full_raw + RS;      // [RS] transform → TMA
+  uint64_t* a_full = empty_raw + RS;        // [AS]   transform → MMA
+  uint64_t* a_empty = a_full + AS;            // [AS]   MMA commit → transform
+  uint64_t* s_full = a_empty + AS;            // [NS]         MMA commit → epilogue
+  uint64_t* s_empty = s_full + TM::NS;              // [NS]         epilogue → MMA
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_empty + TM::NS);
 
-  const int m = a.m, k = a.k;
+  const int m = MT > 0 ? MT : a.m;
+  const int k = a.k;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
-  constexpr uint32_t kCols = kGroups * 2 * KP;  // S[g] = columns [2KP·g, 2KP·(g+1))
-  constexpr uint32_t kTmemCols = kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
   const int nacc = k * m + k;
 
   // ---- setup ----
   if (tid == 0) {
-    for (int s = 0; s < kRawStages; ++s) {
+    for (int s = 0; s < RS; ++s) {
       mbar_init(full_raw + s, 1);
-      mbar_init(empty_raw + s, 4);
+      mbar_init(empty_raw + s, 4);  // the 4 warps of the transform group that consumed it
     }
-    for (int g = 0; g < kGroups; ++g) {
-      mbar_init(op_full + g, 128);
-      mbar_init(s_full + g, 1);
+    for (int s = 0; s < AS; ++s) {
+      mbar_init(a_full + s, 4);
+      mbar_init(a_empty + s, 1);
+    }
+    for (int s = 0; s < TM::NS; ++s) {
+      mbar_init(s_full + s, 1);
+      mbar_init(s_empty + s, 4);
     }
     fence_barrier_init();
   }
-  if (warp == kMmaWarp) tmem_alloc(tmem_holder, kTmemCols);
-  if (warp < kComputeWarps) {
+  if (warp == kMmaWarp) tmem_alloc(tmem_holder, TM::alloc);
+  if (warp < kTransformWarps + kEpiWarps) {
+    const int nthr = (kTransformWarps + kEpiWarps) * 32;
     // B operand rows (already fp16-split and packed by the prep kernel) → SW128 K-major smem
-    for (int i = tid; i < 2 * KP * 8; i += kComputeWarps * 32) {
+    for (int i = tid; i < 2 * KP * 8; i += nthr) {
       const int r = i >> 3, q = i & 7;
       *reinterpret_cast<uint4*>(s_w + sw128(r, q)) = *reinterpret_cast<const uint4*>(a.wop + (size_t)r * 64 + q * 8);
     }
-    // A operand planes zeroed once (chunks beyond the used width stay zero)
-    for (int i = tid; i < kGroups * kTile * 8; i += kComputeWarps * 32)
+    // A operand buffers zeroed once (chunks beyond the used width stay zero)
+    for (int i = tid; i < AS * kTile * 8; i += nthr)
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < nacc; i += kComputeWarps * 32) s_acc[i] = 0ull;
+    for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
+    if (tid == 0) s_qn[0] = 0u;
     fence_proxy_async();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  const float pre = a.pre;
 
   if (warp == kProducerWarp) {
-    // ===================== TMA producer: tile i → raw slot i % kRawStages =====================
+    // ===================== TMA producer: tile i → raw slot i % RS =====================
     if (lane == 0) {
       for (int i = 0; i < my_tiles; ++i) {
-        const int s = i % kRawStages;
-        const int u = i / kRawStages;
+        const int s = i % RS;
+        const int u = i / RS;
         if (u > 0) mbar_wait(empty_raw + s, (u - 1) & 1);
         const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
         const int64_t row0 = t * kTile;
@@ -293,96 +337,72 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       }
     }
   } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (one thread): assign MMAs for whichever group is ready =====================
+    // ===================== MMA issuer (one thread) =====================
     if (lane == 0) {
       const uint32_t a0 = smem_u32(sm + S.off_a), w0 = smem_u32(s_w);
       constexpr uint32_t idesc = idesc_f16(2 * KP);
-      int next[kGroups];
+      for (int i = 0; i < my_tiles; ++i) {
+        const int sa = i % AS, ss = i % TM::NS;
+        mbar_wait(a_full + sa, (i / AS) & 1);
+        if (i >= TM::NS) mbar_wait(s_empty + ss, ((i / TM::NS) - 1) & 1);
+        tc_fence_after();
+        const uint32_t ag = a0 + sa * (kTile * 128);
+        const uint32_t dcol = tmem + ss * 2 * KP;
 #pragma unroll
-      for (int g = 0; g < kGroups; ++g) next[g] = g;
-      int issued = 0;
-      while (issued < my_tiles) {
-#pragma unroll
-        for (int g = 0; g < kGroups; ++g) {
-          const int i = next[g];
-          if (i < my_tiles && mbar_test(op_full + g, (i / kGroups) & 1)) {
-            tc_fence_after();
-            const uint32_t ag = a0 + g * (kTile * 128);
-#pragma unroll
-            for (int ks = 0; ks < L::KSTEPS; ++ks) {
-              if (a.dbg_flags & 2) break;
-              mma_f16(tmem + g * 2 * KP, make_desc(ag + ks * 32, 16, 1024), make_desc(w0 + ks * 32, 16, 1024),
-                      idesc, ks > 0 ? 1u : 0u);
-            }
-            mma_commit(s_full + g);
-            next[g] += kGroups;
-            ++issued;
-          }
+        for (int ks = 0; ks < L::KSTEPS; ++ks) {
+          if (a.dbg_flags & 2) break;
+          mma_f16(dcol, make_desc(ag + ks * 32, 16, 1024), make_desc(w0 + ks * 32, 16, 1024), idesc,
+                  ks > 0 ? 1u : 0u);
         }
+        mma_commit(s_full + ss);   // scores ready
+        mma_commit(a_empty + sa);  // A buffer consumed
       }
     }
-  } else {
-    // ===================== compute warpgroups: thread = point; group g takes tiles i ≡ g (mod 2) =====================
-    const int g = warp >> 2;
-    const int p = tid & 127;                      // row in tile = TMEM lane
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    unsigned char* s_a = sm + S.off_a + g * (kTile * 128);
-    const float pre = a.pre;
-    const float cmaxp = a.cmax[0] * pre;
-    const float scale_f = a.scale_f, err_coef = a.err_coef, err_floor = a.err_floor, nx_inflate = a.nx_inflate;
-    const float inv_pre2 = 1.0f / (pre * pre);
-    const double scale_d = a.scale_d;
-    const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0, full = a.full != 0;
-    const float* __restrict__ gx = a.x;
+  } else if (warp < kTransformWarps) {
+    // ===================== transform: thread = point; group tg takes tiles i ≡ tg (mod 2) =====================
+    const int tg = warp >> 2;
+    const int p = tid & 127;
     const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
     const int key = p & 7;
-    unsigned int my_rechecks = 0, my_changed = 0;
-    for (int i = g; i < my_tiles; i += kGroups) {
-      const int j = i / kGroups;
-      const int s = i % kRawStages;
-      const int u = i / kRawStages;
+    const float* __restrict__ gx = a.x;
+    for (int i = tg; i < my_tiles; i += kTransformGroups) {
+      const int s = i % RS, sa = i % AS;
       const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
       const int64_t row0 = t * kTile;
       const int64_t rem = a.n - row0;
       const int rows = rem < kTile ? (int)rem : kTile;
       const bool active = p < rows;
-      const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && (tid & 127) == 0 && i < 64;
+      const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64;
       long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
       if (stamp) ts[0] = clock64();
-      // previous label (incremental update); issued early to hide its latency
-      const int old = (active && !full) ? __ldg(a.labels + row0 + p) : -1;
-      mbar_wait(full_raw + s, u & 1);
+      mbar_wait(full_raw + s, (i / RS) & 1);
       if (stamp) ts[1] = clock64();
       const float* rs = raw + s * (S.raw_stride / 4);
-      float x[MP];
-      if (rows == kTile) {  // full tile: whole rows inside the bulk copy (12800 B is a multiple of 16)
+      float xs[L::HW];
+      if (rows == kTile) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
+        const float* xr = rs + p * m;
 #pragma unroll
-        for (int f = 0; f < MP; ++f) x[f] = (f < m) ? rs[p * m + f] : 0.f;
+        for (int f = 0; f < L::HW; ++f) {
+          const float v = (f < MP) ? xr[f] : 0.f;
+          xs[f] = (f < m) ? (PRE ? v * pre : v) : 0.f;
+        }
       } else {              // ragged last tile: bulk part + ≤ 3 trailing floats from global
         const uint32_t bulk_elems = (((uint32_t)rows * m * 4u) & ~15u) >> 2;
-#pragma unroll
-        for (int f = 0; f < MP; ++f) {
+        for (int f = 0; f < L::HW; ++f) {
           float v = 0.f;
-          if (f < m && active) {
+          if (f < MP && f < m && active) {
             const uint32_t e = (uint32_t)p * m + f;
-            v = (e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e);
+            v = ((e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e));
+            if (PRE) v *= pre;
           }
-          x[f] = v;
+          xs[f] = v;
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(empty_raw + s);
-      if (stamp) ts[2] = clock64();
-      // --- A row: [xh | xl] fp16, prescaled; feature m carries the ‖c‖² term
-      float xs[L::HW];
-      float nx2 = 0.f;
+      if (lane == 0) mbar_arrive(empty_raw + s);  // raw tile consumed: TMA may refill it
 #pragma unroll
-      for (int f = 0; f < L::HW; ++f) {
-        float v = (f < MP) ? x[f] * pre : 0.f;
-        if (f == m) v = active ? 1.f : 0.f;
-        xs[f] = v;
-        if (f < MP) nx2 = __fmaf_rn(v, (f == m) ? 0.f : v, nx2);
-      }
+      for (int f = 0; f < L::HW; ++f)
+        if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
       uint32_t hw[L::HW / 2], lw[L::HW / 2];
 #pragma unroll
       for (int q = 0; q < L::HW / 2; ++q) {
@@ -392,7 +412,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
       }
-      // row layout (halfs): [0, HW) = xh, [HW, 2HW) = xl; 16-byte chunks of 8 halfs
+      if (stamp) ts[7] = clock64();
+      if (i >= AS) mbar_wait(a_empty + sa, ((i / AS) - 1) & 1);
+      if (stamp) ts[2] = clock64();
+      unsigned char* s_a = sm + S.off_a + sa * (kTile * 128);
 #pragma unroll
       for (int q = 0; q < L::HW / 8; ++q) {
         *reinterpret_cast<uint4*>(s_a + row_off + ((uint32_t)(q ^ key) << 4)) =
@@ -401,90 +424,126 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
       }
       fence_proxy_async();
-      mbar_arrive(op_full + g);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + sa);
       if (stamp) ts[3] = clock64();
-      // --- epilogue: scores from TMEM
-      mbar_wait(s_full + g, j & 1);
+    }
+  } else {
+    // ===================== epilogue groups: thread = point = TMEM lane; group e takes tiles i ≡ e (mod 2) =====================
+    const int ew = warp - kTransformWarps;          // 0..7
+    const int e = ew >> 2;
+    const int p = ((ew & 3) << 5) | lane;          // TMEM lane of this thread
+    const uint32_t lane_base = (uint32_t)((ew & 3) * 32) << 16;
+    const float scale_f = a.scale_f;
+    // certified bound with the dataset's max ‖x‖ (per launch constant, prescaled units)
+    const float tt = (a.xnorm_max + a.cmax[0]) * pre;
+    const float E2 = 2.f * __fmaf_rn(a.err_coef * tt, tt, a.err_floor);
+    const float inv_pre2 = 1.0f / (pre * pre);
+    const double scale_d = a.scale_d;
+    const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0, full = a.full != 0;
+    unsigned int my_changed = 0;
+    auto prev_label = [&](int i) -> int {  // previous label of this thread's point in tile i (or -1)
+      if (full || i >= my_tiles) return -1;
+      const int64_t r = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + p;
+      return r < a.n ? __ldg(a.labels + r) : -1;
+    };
+    int old_next = prev_label(e);
+    for (int i = e; i < my_tiles; i += kEpiGroups) {
+      const int ss = i % TM::NS;
+      const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
+      const int64_t row0 = t * kTile;
+      const int64_t rem = a.n - row0;
+      const int rows = rem < kTile ? (int)rem : kTile;
+      const bool active = p < rows;
+      const int old = old_next;
+      old_next = prev_label(i + kEpiGroups);  // prefetch one tile ahead (global latency off the critical path)
+      const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64;
+      long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
       if (stamp) ts[4] = clock64();
+      mbar_wait(s_full + ss, (i / TM::NS) & 1);
+      if (stamp) ts[5] = clock64();
       tc_fence_after();
-      float sc[KP];
-#pragma unroll
-      for (int c0 = 0; c0 < KP; c0 += 16) {
-        uint32_t r0[16], r1[16];
-        tmem_ld16(tmem + lane_base + g * 2 * KP + c0, r0);
-        tmem_ld16(tmem + lane_base + g * 2 * KP + KP + c0, r1);
-        tmem_ld_wait();
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) sc[c0 + jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
-      }
-      tc_fence_before();  // TMEM reads ordered before the next MMA into S[g]
+      // top-2 over the scores: per 16-column chunk a 4-level tree, then a running merge.
+      // (The filter's argmin tie order is irrelevant: a tie is never certified.)
       float best = __int_as_float(0x7f800000), min2 = best;
       int bi = 0;
 #pragma unroll
-      for (int c = 0; c < KP; ++c) {
-        if (c < k) {
-          if (a.dbg_scores && active) a.dbg_scores[(row0 + p) * k + c] = sc[c] * inv_pre2;
-          const bool lt = sc[c] < best;
-          min2 = lt ? best : fminf(min2, sc[c]);
-          bi = lt ? c : bi;
-          best = lt ? sc[c] : best;
+      for (int c0 = 0; c0 < KP; c0 += 16) {
+        uint32_t r0[16], r1[16];
+        tmem_ld16(tmem + lane_base + ss * 2 * KP + c0, r0);
+        tmem_ld16(tmem + lane_base + ss * 2 * KP + KP + c0, r1);
+        tmem_ld_wait();
+        float v[16], s2[16];
+        int ix[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {  // padded centres (c ≥ k) score +65504: never best or runner-up
+          v[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+          s2[jj] = __int_as_float(0x7f800000);
+          ix[jj] = c0 + jj;
         }
-      }
-      const float tt = __fmaf_rn(sqrtf(nx2), nx_inflate, cmaxp);
-      const float E = __fmaf_rn(err_coef * tt, tt, err_floor);
-      const float thr = best + 2.f * E;
-      int lab = bi;
-      if (active && (exact_only || !(min2 > thr))) {
-        // exact re-decision among the candidates (reference recurrence, ascending c, strict <)
-        ++my_rechecks;
-        double bd = 0.0;
-        int bl = -1;
+        if (a.dbg_scores != nullptr && active) {
 #pragma unroll
-        for (int c = 0; c < KP; ++c) {
-          if (c < k && (exact_only || sc[c] <= thr)) {
-            const double* cc = a.c64 + (size_t)c * m;
-            double acc = 0.0;
+          for (int jj = 0; jj < 16; ++jj)
+            if (c0 + jj < k) a.dbg_scores[(row0 + p) * k + c0 + jj] = v[jj] * inv_pre2;
+        }
 #pragma unroll
-            for (int f = 0; f < MP; ++f) {
-              if (f < m) {
-                const double d = __dsub_rn((double)x[f], cc[f]);
-                acc = __dadd_rn(acc, __dmul_rn(d, d));
-              }
-            }
-            if (bl < 0 || acc < bd) { bd = acc; bl = c; }
+        for (int w = 1; w < 16; w <<= 1) {
+#pragma unroll
+          for (int jj = 0; jj < 16; jj += 2 * w) {
+            const bool rb = v[jj + w] < v[jj];
+            const float lo = rb ? v[jj + w] : v[jj], hi = rb ? v[jj] : v[jj + w];
+            s2[jj] = fminf(hi, fminf(s2[jj], s2[jj + w]));
+            ix[jj] = rb ? ix[jj + w] : ix[jj];
+            v[jj] = lo;
           }
         }
-        lab = bl;
+        const bool rb = v[0] < best;
+        min2 = fminf(rb ? best : v[0], fminf(min2, s2[0]));
+        bi = rb ? ix[0] : bi;
+        best = rb ? v[0] : best;
       }
-      // --- exact incremental update of the per-cluster fixed-point sums
-      if (active && lab != old) {
+      tc_fence_before();  // TMEM reads ordered before the MMA reuses this buffer
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty + ss);
+      const bool certified = !exact_only && (min2 > best + E2);
+      if (active && !certified) {
+        // defer: recheck_kernel re-decides this point exactly and applies its update
+        const unsigned int slot = atomicAdd(s_qn, 1u);
+        if (slot < kQueueCap) {
+          s_q[slot] = row0 + p;
+        } else {  // CTA staging full: straight to the global queue
+          a.recheck_rows[atomicAdd(a.recheck_count, 1u)] = row0 + p;
+        }
+      } else if (active && bi != old) {
+        // --- exact incremental update of the per-cluster fixed-point sums
         ++my_changed;
-        a.labels[row0 + p] = lab;
-#pragma unroll
-        for (int f = 0; f < MP; ++f) {
-          if (f < m) {
-            const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)x[f], scale_d))
-                                           : __float2ll_rn(__fmul_rn(x[f], scale_f));
-            smem_add64(s_acc + (size_t)lab * m + f, (unsigned long long)v);
-            if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
-          }
+        a.labels[row0 + p] = bi;
+        const float* xr = a.x + (row0 + p) * m;  // just streamed: L2 hit
+        for (int f = 0; f < m; ++f) {
+          const float xv = __ldg(xr + f);
+          const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d))
+                                         : __float2ll_rn(__fmul_rn(xv, scale_f));
+          smem_add64(s_acc + (size_t)bi * m + f, (unsigned long long)v);
+          if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
         }
-        smem_add64(s_acc + (size_t)k * m + lab, 1ull);
+        smem_add64(s_acc + (size_t)k * m + bi, 1ull);
         if (old >= 0) smem_add64(s_acc + (size_t)k * m + old, ~0ull);
       }
-      if (stamp) ts[5] = clock64();
+      if (stamp) ts[6] = clock64();
     }
-    unsigned int w1 = my_rechecks, w2 = my_changed;
+    unsigned int w2 = my_changed;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      w1 += __shfl_xor_sync(0xffffffffu, w1, o);
-      w2 += __shfl_xor_sync(0xffffffffu, w2, o);
-    }
-    if (lane == 0 && w1) atomicAdd(&a.st->rechecked, (unsigned long long)w1);
+    for (int o = 16; o > 0; o >>= 1) w2 += __shfl_xor_sync(0xffffffffu, w2, o);
     if (lane == 0 && w2) atomicAdd(&a.st->changed, (unsigned long long)w2);
-    // all compute warps done with their atomics → flush the Δ accumulators (one pass per CTA)
-    asm volatile("bar.sync 1, %0;" ::"r"(kComputeWarps * 32) : "memory");
-    for (int i = tid; i < nacc; i += kComputeWarps * 32) {
+    // all epilogue warps done with their atomics → flush the Δ accumulators and the staged
+    // recheck queue (one global reservation per CTA)
+    asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+    const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
+    if (warp == kTransformWarps && lane == 0) s_qn[1] = qn ? atomicAdd(a.recheck_count, qn) : 0u;
+    asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+    for (unsigned int i = (warp - kTransformWarps) * 32 + lane; i < qn; i += kEpiWarps * 32)
+      a.recheck_rows[s_qn[1] + i] = s_q[i];
+    for (int i = (warp - kTransformWarps) * 32 + lane; i < nacc; i += kEpiWarps * 32) {
       const unsigned long long v = s_acc[i];
       if (v) atomicAdd(a.part + i, v);
     }
@@ -493,8 +552,34 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
-    tmem_dealloc(tmem, kTmemCols);
+    tmem_dealloc(tmem, TM::alloc);
   }
+}
+
+template <int MT, int KP, bool PRE>
+inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_t stream, cudaError_t* ce, char* msg,
+             size_t len) {
+  auto kern = lloyd_pass_tc_kernel<MT, KP, PRE>;
+  constexpr int MP = MT > 0 ? MT : -MT;
+  const size_t smem = TcSmem<MP, KP>(a.m).total;
+  if (smem > smem_optin) {
+    snprintf(msg, len, "tensor-core pass needs %zu B of shared memory (max %zu)", smem, smem_optin);
+    return 2;
+  }
+  cudaError_t c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc smem)"); return 1; }
+  c = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc carveout)"); return 1; }
+  int per_sm = 0;
+  c = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsTC, smem);
+  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "occupancy(tc)"); return 1; }
+  if (per_sm < 1) { snprintf(msg, len, "tensor-core pass does not fit on an SM"); return 2; }
+  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));  // one persistent CTA/SM
+  kern<<<(unsigned)grid, kThreadsTC, smem, stream>>>(a);
+  c = cudaGetLastError();
+  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "lloyd_pass_tc_kernel launch"); return 1; }
+  return 0;
 }
 
 }  // namespace tc

@@ -17,6 +17,7 @@ struct TcArgs {
   int32_t m, k;
   const unsigned short* wop;  // [2KP][64] fp16 B operand rows ([wh|wh], [wl|0]) from the prep/finish kernel
   const float* cmax;       // [0] max ‖fl32(c)‖ (unscaled, rounded up)
+  float xnorm_max;         // max ‖x‖ over the resident points (rounded up)
   const double* c64;       // k × m fp64 centres (exact recheck)
   int32_t* labels;         // in: L_{t-1} (incremental) / out: L_t (written where changed)
   unsigned long long* part;  // Δ (incremental) or full per-cluster fixed-point sums + counts
@@ -28,7 +29,11 @@ struct TcArgs {
   float err_floor;         // absolute floor (prescaled units)
   float nx_inflate;
   int32_t exact_only;
+  int32_t exact_m;         // 1: use a compile-time-m instantiation when one exists for m
+  int32_t prescale;        // 1: multiply x by `pre` (else the data are fp16-safe as is; pre == 1)
   int32_t full;            // 1: old labels invalid (first pass / standalone assign): add every point
+  long long* recheck_rows;      // queue of uncertified points (→ recheck_kernel)
+  unsigned int* recheck_count;
   DevState* st;
   int32_t gate;
   float* dbg_scores;       // optional n × k raw tensor-core scores, unscaled (tests)
@@ -40,6 +45,9 @@ struct TcArgs {
 // (*cuda_err set), 2 if the shape does not fit; msg receives a description.
 int launch(const TcArgs& a, int mp, int kp, int num_sms, size_t smem_optin, cudaStream_t stream,
            cudaError_t* cuda_err, char* msg, size_t msg_len);
+
+// Re-decide the queued points exactly (after launch(), before the finish kernel).
+cudaError_t launch_recheck(const TcArgs& a, int num_sms, cudaStream_t stream);
 
 }  // namespace tc
 }  // namespace km
