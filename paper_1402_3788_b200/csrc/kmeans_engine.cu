@@ -73,6 +73,7 @@ struct km_engine {
   bool next_full = true;            // next TC pass must add every point (no valid previous labels)
   long long* recheck_rows = nullptr;     // queue of uncertified points (n)
   unsigned int* recheck_count = nullptr;
+  unsigned int* cta_done = nullptr;      // fused-finish completion counter
   bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
   int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required
   float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
@@ -204,7 +205,10 @@ static float host_err_coef_tc(int m, int mp) {
   return (float)std::max((m + 8 + 12 * ks) * std::ldexp(1.0, -23), std::ldexp(1.0, -18));
 }
 
-static int launch_tc(km_engine* e, bool full, bool gated) {
+static FinishArgs finish_args(km_engine* e, int mode, bool accumulate);
+static int finish_threads(int k, int m);
+
+static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
   tc::TcArgs a{};
   a.x = (const float*)e->x;
   a.n = e->n;
@@ -232,6 +236,11 @@ static int launch_tc(km_engine* e, bool full, bool gated) {
   a.prescale = e->prescale ? 1 : 0;
   a.recheck_rows = e->recheck_rows;
   a.recheck_count = e->recheck_count;
+  a.fuse_finish = fuse ? 1 : 0;
+  a.cta_done = e->cta_done;
+  a.fin = finish_args(e, 0, !full);
+  a.fin.recheck_rows = e->recheck_rows;  // the fused finish re-decides the overflow queue itself
+  a.fin.full = full ? 1 : 0;
   a.st = e->st;
   a.gate = gated ? 1 : 0;
   a.dbg_scores = e->dbg_scores;
@@ -248,9 +257,12 @@ static int launch_tc(km_engine* e, bool full, bool gated) {
   const int rc = tc::launch(a, mp, e->kp, e->num_sms, e->smem_optin, e->stream, &c, msg, sizeof msg);
   if (rc == 1) return cuda_fail(e, c, msg);
   if (rc == 2) return set_err(e, KM_ERR_CAPACITY, "%s", msg);
-  c = tc::launch_recheck(a, e->num_sms, e->stream);
-  if (c != cudaSuccess) return cuda_fail(e, c, "recheck_kernel launch");
-  e->stats.kernel_launches += 2;
+  e->stats.kernel_launches += 1;
+  if (!fuse) {  // overflow of the per-CTA queues (rare): re-decide before anyone reads the sums
+    c = tc::launch_recheck(a, e->num_sms, e->stream);
+    if (c != cudaSuccess) return cuda_fail(e, c, "recheck_kernel launch");
+    e->stats.kernel_launches += 1;
+  }
   if (a.dbg_times) {
     long long h[64 * 8];
     cudaMemcpyAsync(h, a.dbg_times, sizeof h, cudaMemcpyDeviceToHost, e->stream);
@@ -272,13 +284,13 @@ static int launch_tc(km_engine* e, bool full, bool gated) {
 
 static float host_err_coef(int m) { return (float)((m + 8) * std::ldexp(1.0, -24) * 1.25); }
 
-static int launch_pass(km_engine* e, PassMode mode, bool gated) {
+static int launch_pass(km_engine* e, PassMode mode, bool gated, bool fuse_finish = false) {
   if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
   if (mode != PASS_SUMS_ONLY && use_tc(e)) {
     // the TC pass updates the sums by exact deltas against the previous labels; the first
     // pass of a run (and any standalone assign) adds every point
     const bool full = e->next_full || mode == PASS_ASSIGN_ONLY;
-    const int r = launch_tc(e, full, gated);
+    const int r = launch_tc(e, full, gated, fuse_finish && mode == PASS_ASSIGN_SUMS);
     if (!r && mode == PASS_ASSIGN_SUMS) e->next_full = false;  // tot will track the labels from here on
     e->last_pass_full = full;
     return r;
@@ -336,6 +348,13 @@ static FinishArgs finish_args(km_engine* e, int mode, bool accumulate) {
   f.tot = e->tot;
   f.accumulate = accumulate ? 1 : 0;
   f.recheck_count = e->recheck_count;
+  f.recheck_rows = nullptr;  // standalone finish: the recheck kernel already re-decided the overflow
+  f.x = (const float*)e->x;
+  f.labels = e->labels;
+  f.full = 0;
+  f.scale_d = std::ldexp(1.0, e->frac_bits);
+  f.use_dscale = (e->frac_bits > 120 || e->frac_bits < -120) ? 1 : 0;
+  f.scale_f = f.use_dscale ? 1.0f : (float)f.scale_d;
   f.cur = e->cur;
   f.prev = e->prev;
   f.model_counts = e->model_counts;
@@ -414,11 +433,11 @@ static void free_k(km_engine* e) {
   dfree(e->labels); dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
   dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->d2); dfree(e->partials); dfree(e->winner);
   dfree(e->scratch_d); dfree(e->labels64); dfree(e->wop); dfree(e->tot); dfree(e->recheck_rows);
-  dfree(e->recheck_count);
+  dfree(e->recheck_count); dfree(e->cta_done);
   e->labels = nullptr; e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
   e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->d2 = nullptr; e->partials = nullptr; e->winner = nullptr;
   e->scratch_d = nullptr; e->labels64 = nullptr; e->wop = nullptr; e->tot = nullptr;
-  e->recheck_rows = nullptr; e->recheck_count = nullptr;
+  e->recheck_rows = nullptr; e->recheck_count = nullptr; e->cta_done = nullptr;
   e->k = 0;
   e->kp = 0;
 }
@@ -450,6 +469,8 @@ static int ensure_k(km_engine* e, int32_t k) {
   if ((r = dalloc(e, &e->recheck_rows, 8 * (size_t)e->n))) return r;
   if ((r = dalloc(e, &e->recheck_count, 16))) return r;
   CK(cudaMemsetAsync(e->recheck_count, 0, 16, e->stream));
+  if ((r = dalloc(e, &e->cta_done, 16))) return r;
+  CK(cudaMemsetAsync(e->cta_done, 0, 16, e->stream));
   CK(cudaMemsetAsync(e->tot, 0, 8 * ((size_t)k * m + k), e->stream));
   e->next_full = true;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * m + k), e->stream));
@@ -880,32 +901,36 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
   if ((r = launch_prep(e))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   e->next_full = true;  // the labels buffer does not hold L of this run yet
+  // Tensor-core path: ONE launch per iteration — pass t + (last CTA) finish t+1.
+  // SIMT path: finish and pass are separate launches.
+  const bool fused = use_tc(e);
   bool prev_full = true;
   int batch = 1;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timed;
   auto timed_pass = [&](void) -> int {
-    if (!e->profiling) {
-      const int rr = launch_pass(e, PASS_ASSIGN_SUMS, true);
-      prev_full = e->last_pass_full;
-      return rr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (e->profiling) {
+      const size_t need = 2 * (timed.size() + 1);
+      while (e->ev.size() < need) {
+        cudaEvent_t ev;
+        CK(cudaEventCreate(&ev));
+        e->ev.push_back(ev);
+      }
+      a = e->ev[need - 2];
+      b = e->ev[need - 1];
+      CK(cudaEventRecord(a, e->stream));
     }
-    const size_t need = 2 * (timed.size() + 1);
-    while (e->ev.size() < need) {
-      cudaEvent_t ev;
-      CK(cudaEventCreate(&ev));
-      e->ev.push_back(ev);
-    }
-    cudaEvent_t a = e->ev[need - 2], b = e->ev[need - 1];
-    CK(cudaEventRecord(a, e->stream));
-    int rr = launch_pass(e, PASS_ASSIGN_SUMS, true);
+    const int rr = launch_pass(e, PASS_ASSIGN_SUMS, true, fused);
     if (rr) return rr;
     prev_full = e->last_pass_full;
-    CK(cudaEventRecord(b, e->stream));
-    timed.push_back({a, b});
+    if (e->profiling) {
+      CK(cudaEventRecord(b, e->stream));
+      timed.push_back({a, b});
+    }
     return KM_OK;
   };
-  // account the passes of a batch that actually ran (gated passes after
-  // done / need_host exit immediately and are not counted)
+  // account the passes of a batch that actually ran (gated launches after done / need_host
+  // exit immediately and are not counted)
   auto account = [&](int n_ran) -> int {
     for (int i = 0; i < (int)timed.size() && i < n_ran; ++i) {
       float ms = 0.f;
@@ -916,31 +941,43 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
     timed.clear();
     return KM_OK;
   };
-  // L0 = A(C0) (engine.py:328), fused with the sums U(L0) needs.
+  // L0 = A(C0) (engine.py:328), fused with the sums U(L0) needs (and, fused, the first update).
   if ((r = timed_pass())) return r;
   int first = 1;
   int t_before = 0;
   for (;;) {
     for (int b = 0; b < batch; ++b) {
-      if ((r = launch_finish(e, 0, !prev_full))) return r;
+      if (!fused && (r = launch_finish(e, 0, !prev_full))) return r;
       if ((r = timed_pass())) return r;
     }
     if ((r = read_state(e))) return r;
     const DevState s = *e->st_host;
     const int ran_updates = s.t - t_before;
-    const int stopped = (s.done && s.converged) || s.need_host ? 1 : 0;
-    if ((r = account(first + std::max(0, ran_updates - stopped)))) return r;
+    int ran;
+    if (fused) {  // launch j = pass j + finish j+1; the exhausted final launch folds without t += 1
+      ran = ran_updates + ((s.done && !s.converged) ? 1 : 0);
+    } else {
+      const int stopped = (s.done && s.converged) || s.need_host ? 1 : 0;
+      ran = first + std::max(0, ran_updates - stopped);
+    }
+    if ((r = account(ran))) return r;
     first = 0;
     t_before = s.t;
     if (s.done) break;
     if (s.need_host) {
       if ((r = repair_local(e))) return r;
       if ((r = launch_check(e))) return r;
-      if ((r = timed_pass())) return r;
-      // the check may have finished the loop (converged): then the pass was gated
-      if ((r = read_state(e))) return r;
-      if ((r = account(e->st_host->done ? 0 : 1))) return r;
-      if (e->st_host->done) break;
+      if (!fused) {
+        if ((r = timed_pass())) return r;
+        // the check may have finished the loop (converged): then the pass was gated
+        if ((r = read_state(e))) return r;
+        if ((r = account(e->st_host->done ? 0 : 1))) return r;
+        if (e->st_host->done) break;
+      } else {
+        if ((r = read_state(e))) return r;
+        if (e->st_host->done) break;
+        t_before = e->st_host->t;
+      }
       batch = 1;
       continue;
     }

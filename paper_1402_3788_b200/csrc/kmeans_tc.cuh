@@ -398,8 +398,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           xs[f] = v;
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_raw + s);  // raw tile consumed: TMA may refill it
 #pragma unroll
       for (int f = 0; f < L::HW; ++f)
         if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
@@ -412,6 +410,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
         lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
       }
+      // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
+      // the TMA producer may refill it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_raw + s);
       if (stamp) ts[7] = clock64();
       if (i >= AS) mbar_wait(a_empty + sa, ((i / AS) - 1) & 1);
       if (stamp) ts[2] = clock64();
@@ -535,24 +537,57 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) w2 += __shfl_xor_sync(0xffffffffu, w2, o);
     if (lane == 0 && w2) atomicAdd(&a.st->changed, (unsigned long long)w2);
-    // all epilogue warps done with their atomics → flush the Δ accumulators and the staged
-    // recheck queue (one global reservation per CTA)
-    asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
-    const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
-    if (warp == kTransformWarps && lane == 0) s_qn[1] = qn ? atomicAdd(a.recheck_count, qn) : 0u;
-    asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
-    for (unsigned int i = (warp - kTransformWarps) * 32 + lane; i < qn; i += kEpiWarps * 32)
-      a.recheck_rows[s_qn[1] + i] = s_q[i];
-    for (int i = (warp - kTransformWarps) * 32 + lane; i < nacc; i += kEpiWarps * 32) {
-      const unsigned long long v = s_acc[i];
-      if (v) atomicAdd(a.part + i, v);
-    }
   }
+  // ===================== tail (all warps) =====================
   tc_fence_before();
-  __syncthreads();
+  __syncthreads();  // every role done: Δ atomics and the CTA's recheck queue are complete
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, TM::alloc);
+  }
+  {
+    // exact re-decision of this CTA's uncertified points (warp per point), Δ into s_acc
+    const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
+    const bool full = a.full != 0;
+    for (unsigned int q = warp; q < qn; q += kThreadsTC / 32) {
+      const long long row = s_q[q];
+      const float xl = lane < m ? __ldg(a.x + row * m + lane) : 0.f;
+      const int bl = exact_label_warp(xl, m, k, a.c64);
+      const int old = full ? -1 : a.labels[row];
+      if (bl != old) {
+        if (lane == 0) {
+          a.labels[row] = bl;
+          smem_add64(s_acc + (size_t)k * m + bl, 1ull);
+          if (old >= 0) smem_add64(s_acc + (size_t)k * m + old, ~0ull);
+          if (!full) atomicAdd(&a.st->changed, 1ull);
+        }
+        if (lane < m) {
+          const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xl, a.scale_d))
+                                           : __float2ll_rn(__fmul_rn(xl, a.scale_f));
+          smem_add64(s_acc + (size_t)bl * m + lane, (unsigned long long)v);
+          if (old >= 0) smem_add64(s_acc + (size_t)old * m + lane, (unsigned long long)(-v));
+        }
+      }
+    }
+    if (tid == 0 && qn) atomicAdd(&a.st->rechecked, (unsigned long long)qn);
+  }
+  __syncthreads();
+  for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
+    const unsigned long long v = s_acc[i];
+    if (v) atomicAdd(a.part + i, v);
+  }
+  if (a.fuse_finish) {
+    // the last CTA to arrive runs the finish of this iteration (no separate launch)
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(a.cta_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      finish_block(a.fin);
+      if (tid == 0) *a.cta_done = 0u;
+    }
   }
 }
 

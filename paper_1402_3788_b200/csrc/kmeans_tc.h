@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "kmeans_state.h"
+#include "kmeans_finish.cuh"
 
 namespace km {
 namespace tc {
@@ -32,8 +33,11 @@ struct TcArgs {
   int32_t exact_m;         // 1: use a compile-time-m instantiation when one exists for m
   int32_t prescale;        // 1: multiply x by `pre` (else the data are fp16-safe as is; pre == 1)
   int32_t full;            // 1: old labels invalid (first pass / standalone assign): add every point
-  long long* recheck_rows;      // queue of uncertified points (→ recheck_kernel)
+  long long* recheck_rows;      // global overflow queue of uncertified points
   unsigned int* recheck_count;
+  int32_t fuse_finish;     // 1: the last CTA to finish runs finish_block(fin) (single-GPU loop)
+  unsigned int* cta_done;  // completion counter for the fused finish (self-resetting)
+  FinishArgs fin;
   DevState* st;
   int32_t gate;
   float* dbg_scores;       // optional n × k raw tensor-core scores, unscaled (tests)

@@ -76,3 +76,23 @@ def test_headline_shape_uses_tensor_cores():
     eng.lloyd(x[:16].astype(np.float64), 2, 0.0)
     assert eng.kernel_path() == 2
     eng.close()
+
+
+def test_filter_scores_full_size_no_races():
+    """Every tensor-core score of a 2M-point pass (≈15.6k tiles through the TMA / transform /
+    MMA / epilogue rings) is within the certified bound: a ring race shows up as rows scored
+    with another point's coordinates."""
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    n, m, k = 2_000_000, 25, 16
+    x = generate_synthetic_array(n, m, k, seed=5, dtype=np.float32)
+    c = x[:k].astype(np.float64) + 0.25
+    eng = native().NativeEngine(0)
+    eng.load(x)
+    got = eng.debug_filter_scores(c)
+    eng.close()
+    want = exact_scores(x, c)
+    nx = np.sqrt((x.astype(np.float64) ** 2).sum(1))
+    cmax = np.sqrt((c.astype(np.float32).astype(np.float64) ** 2).sum(1)).max()
+    ratio = np.abs(got - want) / ((nx + cmax) ** 2)[:, None]
+    assert float(ratio.max()) <= max((m + 8 + 48) * 2.0 ** -23, 2.0 ** -18) / 4
