@@ -248,8 +248,8 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
   a.dbg_times = nullptr;
   if (getenv("KM_TC_TIMES")) {  // tuning only: dump per-tile stamps of CTA 0 to a file after the pass
     static long long* dt = nullptr;
-    if (!dt) cudaMalloc((void**)&dt, 64 * 8 * 8);
-    cudaMemsetAsync(dt, 0, 64 * 8 * 8, e->stream);
+    if (!dt) cudaMalloc((void**)&dt, 1024 * 8 * 8);
+    cudaMemsetAsync(dt, 0, 1024 * 8 * 8, e->stream);
     a.dbg_times = dt;
   }
   char msg[256] = {0};
@@ -264,7 +264,7 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
     e->stats.kernel_launches += 1;
   }
   if (a.dbg_times) {
-    long long h[64 * 8];
+    static long long h[1024 * 8];
     cudaMemcpyAsync(h, a.dbg_times, sizeof h, cudaMemcpyDeviceToHost, e->stream);
     cudaStreamSynchronize(e->stream);
     FILE* f = fopen(getenv("KM_TC_TIMES"), "a");
@@ -274,6 +274,35 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
         const long long* t = h + i * 8;  // transform: raw wait, compute, A-buffer wait, store; epilogue: s wait, body
         fprintf(f, "tile %2d  T: raw %5lld comp %5lld awaitA %5lld sts %5lld | E: swait %5lld body %5lld | t0 %lld\n", i,
                 t[1] - t[0], t[7] - t[1], t[2] - t[7], t[3] - t[2], t[5] - t[4], t[6] - t[5], t[0] - h[0]);
+      }
+      for (int b = 0; b < 64; ++b) {  // per-CTA phases: main loop, wait all roles, tail recheck, flush, finish
+        const long long* t = h + 64 * 8 + b * 8;
+        if (!t[7] || b > 8 && !t[6]) continue;
+        fprintf(f, "cta %2d main %7lld  sync %6lld  recheck(%lld) %6lld  flush %6lld  finish %7lld%s\n", b,
+                t[0] - t[7], t[1] - t[0], t[5], t[2] - t[1], t[3] - t[2], t[6] ? t[4] - t[3] : 0LL, t[6] ? " <- last" : "");
+      }
+      for (int b = 0; b < 64; ++b) {
+        const long long* t = h + 64 * 8 + b * 8 + 8 * 64;
+        if (t[0] && t[5]) fprintf(f, "finish(cta %d): head %lld fold %lld divide %lld empties %lld check+prep %lld\n", b,
+                                  t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
+      }
+      for (int b = 0; b < 8; ++b) {
+        const long long* r = h + 2048 + b * 8;
+        const long long* t = h + 64 * 8 + b * 8;
+        if (r[0]) fprintf(f, "recheck cta %d: staged %lld  xload %lld  compute %lld  rest %lld  end->sync %lld\n", b,
+                          r[0] - t[1], r[1] - r[0], r[2] - r[1], r[3] - r[2], t[2] - r[3]);
+      }
+      {
+        long long e0 = 0, e1 = 0, m1 = 0, m0 = 0, t1 = 0, x1 = 0;
+        for (int b = 0; b < 1024; ++b) {
+          const long long* g = h + 4096 + b * 4;
+          if (!g[0]) break;
+          e0 = e0 ? std::min(e0, g[0]) : g[0]; e1 = std::max(e1, g[0]);
+          m0 = m0 ? std::min(m0, g[1]) : g[1]; m1 = std::max(m1, g[1]);
+          t1 = std::max(t1, g[2]); x1 = std::max(x1, g[3]);
+        }
+        fprintf(f, "gtimer(ns from first entry): last entry %lld  main end min %lld max %lld  tail end max %lld  exit max %lld\n",
+                e1 - e0, m0 - e0, m1 - e0, t1 - e0, x1 - e0);
       }
       fprintf(f, "----\n");
       fclose(f);
@@ -382,7 +411,8 @@ static int finish_threads(int k, int m) {
 
 static int launch_finish(km_engine* e, int mode, bool accumulate) {
   FinishArgs f = finish_args(e, mode, accumulate);
-  lloyd_finish_kernel<<<1, finish_threads(e->k, e->m), 0, e->stream>>>(f);
+  const int cap = 2 * e->k * e->m <= 6144 ? 2 * e->k * e->m : 0;  // stage C_{t-1}, C_t in ≤ 48 KB
+  lloyd_finish_kernel<<<1, finish_threads(e->k, e->m), (size_t)cap * 8, e->stream>>>(f, cap);
   CK_LAUNCH("lloyd_finish_kernel launch");
   e->stats.kernel_launches += 1;
   return KM_OK;

@@ -12,17 +12,20 @@ namespace km {
 // Exact re-decision of one point by a warp: the reference recurrence (_kernels.py:31-44:
 // features ascending, d = x − c, acc += d·d, no FMA) per centre, lane = centre, argmin with the
 // lowest index on ties.  x_lane holds feature `lane` (m ≤ 32).  Returns the label (all lanes).
+template <int MMAX = 32>
 __device__ __forceinline__ int exact_label_warp(float x_lane, int m, int k, const double* __restrict__ c64) {
   const int lane = threadIdx.x & 31;
   double bd = 0.0;
   int bl = -1;
   for (int c0 = 0; c0 < k; c0 += 32) {
     const int c = c0 + lane;
+    const int cl = c < k ? c : 0;
     double acc = 0.0;
-    for (int f = 0; f < m; ++f) {
-      const double xv = (double)__shfl_sync(0xffffffffu, x_lane, f);
-      if (c < k) {
-        const double d = __dsub_rn(xv, c64[(size_t)c * m + f]);
+#pragma unroll
+    for (int f = 0; f < MMAX; ++f) {  // unrolled: centre loads issue up front; fp64 chain in feature order
+      if (f < m) {
+        const double xv = (double)__shfl_sync(0xffffffffu, x_lane, f);
+        const double d = __dsub_rn(xv, c64[(size_t)cl * m + f]);
         acc = __dadd_rn(acc, __dmul_rn(d, d));
       }
     }
@@ -34,6 +37,51 @@ __device__ __forceinline__ int exact_label_warp(float x_lane, int m, int k, cons
     if (ol >= 0 && (bl < 0 || od < bd || (od == bd && ol < bl))) { bd = od; bl = ol; }
   }
   return bl;
+}
+
+// NB points per warp at once (lane = centre): the centre coordinate is loaded once
+// per feature and NB independent fp64 chains hide the DADD latency; each chain is
+// still the reference's exact sequential recurrence.
+template <int MMAX, int NB>
+__device__ __forceinline__ void exact_label_warp_batch(const float (&x_lane)[NB], int m, int k,
+                                                       const double* __restrict__ c64, int (&label)[NB]) {
+  const int lane = threadIdx.x & 31;
+  double bd[NB];
+  int bl[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) { bd[j] = 0.0; bl[j] = -1; }
+  for (int c0 = 0; c0 < k; c0 += 32) {
+    const int c = c0 + lane;
+    const int cl = c < k ? c : 0;
+    double acc[NB];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int f = 0; f < MMAX; ++f) {
+      if (f < m) {
+        const double cv = c64[(size_t)cl * m + f];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const double d = __dsub_rn((double)__shfl_sync(0xffffffffu, x_lane[j], f), cv);
+          acc[j] = __dadd_rn(acc[j], __dmul_rn(d, d));
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j)
+      if (c < k && (bl[j] < 0 || acc[j] < bd[j])) { bd[j] = acc[j]; bl[j] = c; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const double od = __shfl_xor_sync(0xffffffffu, bd[j], o);
+      const int ol = __shfl_xor_sync(0xffffffffu, bl[j], o);
+      if (ol >= 0 && (bl[j] < 0 || od < bd[j] || (od == bd[j] && ol < bl[j]))) { bd[j] = od; bl[j] = ol; }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NB; ++j) label[j] = bl[j];
 }
 
 // ---------------------------------------------------------------------------
@@ -141,10 +189,13 @@ __device__ __forceinline__ int block_converged(const double* __restrict__ prev, 
   return w <= tol ? 1 : 0;
 }
 
-__device__ __forceinline__ void loop_check(FinishArgs& a, double* s_redd, float* s_red) {
+__device__ __forceinline__ void loop_check(FinishArgs& a, double* s_redd, float* s_red, const double* prev_s = nullptr,
+                                           const double* cur_s = nullptr) {
   DevState* st = a.st;
-  const int conv = block_converged(a.prev, a.cur, a.k, a.m, st->tol, s_redd);
-  block_prep_filter(a.cur, a.w, a.cn, a.cmax, a.k, a.m, a.mpad, s_red, a.wop, a.kp, a.pre);
+  const double* P = prev_s ? prev_s : a.prev;
+  const double* C = cur_s ? cur_s : a.cur;
+  const int conv = block_converged(P, C, a.k, a.m, st->tol, s_redd);
+  block_prep_filter(C, a.w, a.cn, a.cmax, a.k, a.m, a.mpad, s_red, a.wop, a.kp, a.pre);
   if (threadIdx.x == 0) {
     st->need_host = 0;
     if (conv) {
@@ -186,7 +237,12 @@ __device__ __forceinline__ void recheck_global_queue(FinishArgs& a) {
 
 // Block-level finish (any block size that is a multiple of 32, ≤ 1024).  Runs as its own
 // one-CTA kernel after a pass, or in the last CTA of the fused tensor-core pass.
-static __device__ __noinline__ void finish_block(FinishArgs a) {
+// `stage` (shared memory, `stage_cap` doubles) holds C_{t-1} and C_t while the congruence test and
+// the filter prep read them (global memory otherwise).
+static __device__ __noinline__ void finish_block(FinishArgs a, double* stage, int stage_cap,
+                                                long long* fts = nullptr) {
+#define FTS(i) do { if (fts != nullptr && threadIdx.x == 0) fts[i] = clock64(); } while (0)
+  FTS(0);
   __shared__ float s_red[32];
   __shared__ double s_redd[32];
   __shared__ int s_empty[32];
@@ -212,26 +268,32 @@ static __device__ __noinline__ void finish_block(FinishArgs a) {
       return;
     }
   }
+  FTS(1);
   // running totals of the current labels (exact integer arithmetic: Δ-updates == recomputation)
   for (int i = threadIdx.x; i < k * m + k; i += blockDim.x) {
     a.tot[i] = a.accumulate ? a.tot[i] + a.part[i] : a.part[i];
     a.part[i] = 0ull;
   }
   __syncthreads();
+  FTS(2);
   unsigned long long* sums = a.tot;
   unsigned long long* cnts = a.tot + (size_t)k * m;
   // prev ← cur ; cur ← S/N  (engine._finish_update, engine.py:249-263)
+  const bool staged = stage != nullptr && 2 * k * m <= stage_cap;
   for (int i = threadIdx.x; i < k * m; i += blockDim.x) {
     const int cc = i / m;
     const long long nc = (long long)cnts[cc];
-    a.prev[i] = a.cur[i];
-    if (nc > 0) {
-      const double s = __dmul_rn((double)(long long)sums[i], a.inv_scale);
-      a.cur[i] = __ddiv_rn(s, (double)nc);
-    } else {
-      a.cur[i] = 0.0;  // placeholder; every empty cluster is re-seeded by the repair
+    const double old = a.cur[i];
+    double v = 0.0;  // placeholder for empty clusters; every one is re-seeded by the repair
+    if (nc > 0) v = __ddiv_rn(__dmul_rn((double)(long long)sums[i], a.inv_scale), (double)nc);
+    a.prev[i] = old;
+    a.cur[i] = v;
+    if (staged) {
+      stage[i] = old;
+      stage[k * m + i] = v;
     }
   }
+  FTS(3);
   int empties = 0;
   for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
     const long long nc = (long long)cnts[cc];
@@ -256,7 +318,10 @@ static __device__ __noinline__ void finish_block(FinishArgs a) {
     if (threadIdx.x == 0) st->need_host = 1;
     return;
   }
-  loop_check(a, s_redd, s_red);
+  FTS(4);
+  loop_check(a, s_redd, s_red, staged ? stage : nullptr, staged ? stage + k * m : nullptr);
+  FTS(5);
+#undef FTS
 }
 
 

@@ -278,7 +278,10 @@ __global__ void __launch_bounds__(kThreads) lloyd_pass_kernel(PassArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a) { finish_block(a); }
+__global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a, int stage_cap) {
+  extern __shared__ double s_stage[];
+  finish_block(a, stage_cap > 0 ? s_stage : nullptr, stage_cap);
+}
 
 
 // After a host-driven repair: congruence test + prep (no division).

@@ -211,6 +211,12 @@ __host__ __device__ constexpr uint32_t idesc_u8_amn(int n) {
 }
 
 // byte offset of 16-B chunk q of row r inside a SW128 region (8-row atoms of 1 KiB)
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __device__ __forceinline__ uint32_t sw128(int r, int q) {
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + (((q ^ (r & 7)) & 7) << 4));
 }
@@ -281,6 +287,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
   const int nacc = k * m + k;
+  if (a.dbg_times != nullptr && tid == 0) {
+    a.dbg_times[64 * 8 + (blockIdx.x % 64) * 8 + 7] = clock64();
+    a.dbg_times[4096 + blockIdx.x * 4] = (long long)globaltimer();
+  }
 
   // ---- setup ----
   if (tid == 0) {
@@ -512,7 +522,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         // defer: recheck_kernel re-decides this point exactly and applies its update
         const unsigned int slot = atomicAdd(s_qn, 1u);
         if (slot < kQueueCap) {
-          s_q[slot] = row0 + p;
+          s_q[slot] = ((row0 + p) << 24) | (long long)(old + 1);  // row | previous label (+1; 0 = none)
         } else {  // CTA staging full: straight to the global queue
           a.recheck_rows[atomicAdd(a.recheck_count, 1u)] = row0 + p;
         }
@@ -539,39 +549,74 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (lane == 0 && w2) atomicAdd(&a.st->changed, (unsigned long long)w2);
   }
   // ===================== tail (all warps) =====================
+  long long* tstamp = (a.dbg_times != nullptr && tid == 0) ? a.dbg_times + 64 * 8 + (blockIdx.x % 64) * 8 : nullptr;
+  if (tstamp) tstamp[0] = clock64();
+  if (a.dbg_times != nullptr && tid == 0) a.dbg_times[4096 + blockIdx.x * 4 + 1] = (long long)globaltimer();
   tc_fence_before();
   __syncthreads();  // every role done: Δ atomics and the CTA's recheck queue are complete
+  if (tstamp) tstamp[1] = clock64();
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, TM::alloc);
   }
+  // the raw ring is free now: stage the fp64 centres there for the recheck (and the finish)
+  double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
+  const int stage_cap = (int)(RS * S.raw_stride / 8);
+  const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
+  const bool c_staged = k * m <= stage_cap;
+  if (qn && c_staged) {
+    for (int i = tid; i < k * m; i += kThreadsTC) s_stage[i] = a.c64[i];
+    __syncthreads();
+  }
+  long long* rst = (a.dbg_times != nullptr && lane == 0 && warp == 0) ? a.dbg_times + 2048 + (blockIdx.x % 64) * 8 : nullptr;
+  if (rst) rst[0] = clock64();
   {
     // exact re-decision of this CTA's uncertified points (warp per point), Δ into s_acc
-    const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
     const bool full = a.full != 0;
-    for (unsigned int q = warp; q < qn; q += kThreadsTC / 32) {
-      const long long row = s_q[q];
-      const float xl = lane < m ? __ldg(a.x + row * m + lane) : 0.f;
-      const int bl = exact_label_warp(xl, m, k, a.c64);
-      const int old = full ? -1 : a.labels[row];
-      if (bl != old) {
-        if (lane == 0) {
-          a.labels[row] = bl;
-          smem_add64(s_acc + (size_t)k * m + bl, 1ull);
-          if (old >= 0) smem_add64(s_acc + (size_t)k * m + old, ~0ull);
-          if (!full) atomicAdd(&a.st->changed, 1ull);
-        }
-        if (lane < m) {
-          const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xl, a.scale_d))
-                                           : __float2ll_rn(__fmul_rn(xl, a.scale_f));
-          smem_add64(s_acc + (size_t)bl * m + lane, (unsigned long long)v);
-          if (old >= 0) smem_add64(s_acc + (size_t)old * m + lane, (unsigned long long)(-v));
+    const double* C = c_staged ? s_stage : a.c64;
+    // batches of 4 points per warp: their x rows (one feature per lane) are fetched together
+    for (unsigned int q0 = warp * 4; q0 < qn; q0 += (kThreadsTC / 32) * 4) {
+      long long ent[4];
+      float xb[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        ent[j] = (q0 + j < qn) ? s_q[q0 + j] : -1;
+        xb[j] = (ent[j] >= 0 && lane < m) ? __ldg(a.x + (ent[j] >> 24) * m + lane) : 0.f;
+      }
+      if (rst && q0 == 0) { rst[1] = clock64() + (long long)(xb[0] + xb[1] + xb[2] + xb[3] == 12345.f); }
+      int lb[4];
+      exact_label_warp_batch<MP, 4>(xb, m, k, C, lb);
+      if (rst && q0 == 0) { rst[2] = clock64() + (lb[0] + lb[1] + lb[2] + lb[3] == 12345); }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (ent[j] < 0) continue;
+        const long long row = ent[j] >> 24;
+        const float xl = xb[j];
+        const int bl = lb[j];
+        const int old = full ? -1 : (int)(ent[j] & 0xffffff) - 1;
+        if (bl != old) {
+          if (lane == 0) {
+            a.labels[row] = bl;
+            smem_add64(s_acc + (size_t)k * m + bl, 1ull);
+            if (old >= 0) smem_add64(s_acc + (size_t)k * m + old, ~0ull);
+            if (!full) atomicAdd(&a.st->changed, 1ull);
+          }
+          if (lane < m) {
+            const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xl, a.scale_d))
+                                             : __float2ll_rn(__fmul_rn(xl, a.scale_f));
+            smem_add64(s_acc + (size_t)bl * m + lane, (unsigned long long)v);
+            if (old >= 0) smem_add64(s_acc + (size_t)old * m + lane, (unsigned long long)(-v));
+          }
         }
       }
     }
+    if (rst) rst[3] = clock64();
     if (tid == 0 && qn) atomicAdd(&a.st->rechecked, (unsigned long long)qn);
+    if (tstamp) tstamp[5] = qn;
   }
   __syncthreads();
+  if (tstamp) tstamp[2] = clock64();
+  if (a.dbg_times != nullptr && tid == 0) a.dbg_times[4096 + blockIdx.x * 4 + 2] = (long long)globaltimer();
   for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
     const unsigned long long v = s_acc[i];
     if (v) atomicAdd(a.part + i, v);
@@ -583,12 +628,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     __syncthreads();
     if (tid == 0) s_last = atomicAdd(a.cta_done, 1u) == gridDim.x - 1;
     __syncthreads();
+    if (tstamp) tstamp[3] = clock64();
     if (s_last) {
       __threadfence();
-      finish_block(a.fin);
+      finish_block(a.fin, s_stage, stage_cap, tstamp ? tstamp + 8 * 64 : nullptr);
       if (tid == 0) *a.cta_done = 0u;
+      if (tstamp) { tstamp[4] = clock64(); tstamp[6] = 1; }
     }
   }
+  if (a.dbg_times != nullptr && tid == 0) a.dbg_times[4096 + blockIdx.x * 4 + 3] = (long long)globaltimer();
 }
 
 template <int MT, int KP, bool PRE>
