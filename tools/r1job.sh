@@ -1,0 +1,7 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/r1_smi.txt
+python bench.py > gpurun_out/r1_bench.json 2> gpurun_out/r1_bench.err
+python bench.py --impl reference > gpurun_out/r1_bench_ref.json 2> gpurun_out/r1_bench_ref.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r1_launches.csv python bench.py --steps 20 --warmup 3 --skip-e2e --skip-cpu --max-reps 1 > gpurun_out/r1_ncu_launch.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:lloyd_pass_tc -s 40 -c 1 -o gpurun_out/r1_tc_full python tools/profile_pass.py cfg3 50 > gpurun_out/r1_ncu_full.log 2>&1
+ls -la gpurun_out
