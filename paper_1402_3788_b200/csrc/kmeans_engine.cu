@@ -74,6 +74,8 @@ struct km_engine {
   long long* recheck_rows = nullptr;     // queue of uncertified points (n)
   unsigned int* recheck_count = nullptr;
   unsigned int* cta_done = nullptr;      // fused-finish completion counter
+  unsigned int* grid_sync = nullptr;     // resident loop: barrier arrivals, totals consumed
+  bool resident_unfit = false;           // the resident TC loop does not fit this shape (use per-iteration launches)
   bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
   int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required
   float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
@@ -208,7 +210,10 @@ static float host_err_coef_tc(int m, int mp) {
 static FinishArgs finish_args(km_engine* e, int mode, bool accumulate);
 static int finish_threads(int k, int m);
 
-static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
+// resident: the whole Lloyd loop in one cooperative launch (returns KM_RESIDENT_UNFIT when the
+// shape only fits the launch-per-iteration kernel)
+constexpr int KM_RESIDENT_UNFIT = -3;
+static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, bool resident = false) {
   tc::TcArgs a{};
   a.x = (const float*)e->x;
   a.n = e->n;
@@ -241,6 +246,9 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
   a.fin = finish_args(e, 0, !full);
   a.fin.recheck_rows = e->recheck_rows;  // the fused finish re-decides the overflow queue itself
   a.fin.full = full ? 1 : 0;
+  a.resident = resident ? 1 : 0;
+  a.grid_sync = e->grid_sync;
+  if (resident) CK(cudaMemsetAsync(e->grid_sync, 0, 16, e->stream));
   a.st = e->st;
   a.gate = gated ? 1 : 0;
   a.dbg_scores = e->dbg_scores;
@@ -257,8 +265,9 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
   const int rc = tc::launch(a, mp, e->kp, e->num_sms, e->smem_optin, e->stream, &c, msg, sizeof msg);
   if (rc == 1) return cuda_fail(e, c, msg);
   if (rc == 2) return set_err(e, KM_ERR_CAPACITY, "%s", msg);
+  if (rc == 3) return KM_RESIDENT_UNFIT;
   e->stats.kernel_launches += 1;
-  if (!fuse) {  // overflow of the per-CTA queues (rare): re-decide before anyone reads the sums
+  if (!fuse && !resident) {  // overflow of the per-CTA queues (rare): re-decide before anyone reads the sums
     c = tc::launch_recheck(a, e->num_sms, e->stream);
     if (c != cudaSuccess) return cuda_fail(e, c, "recheck_kernel launch");
     e->stats.kernel_launches += 1;
@@ -274,35 +283,6 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false) {
         const long long* t = h + i * 8;  // transform: raw wait, compute, A-buffer wait, store; epilogue: s wait, body
         fprintf(f, "tile %2d  T: raw %5lld comp %5lld awaitA %5lld sts %5lld | E: swait %5lld body %5lld | t0 %lld\n", i,
                 t[1] - t[0], t[7] - t[1], t[2] - t[7], t[3] - t[2], t[5] - t[4], t[6] - t[5], t[0] - h[0]);
-      }
-      for (int b = 0; b < 64; ++b) {  // per-CTA phases: main loop, wait all roles, tail recheck, flush, finish
-        const long long* t = h + 64 * 8 + b * 8;
-        if (!t[7] || b > 8 && !t[6]) continue;
-        fprintf(f, "cta %2d main %7lld  sync %6lld  recheck(%lld) %6lld  flush %6lld  finish %7lld%s\n", b,
-                t[0] - t[7], t[1] - t[0], t[5], t[2] - t[1], t[3] - t[2], t[6] ? t[4] - t[3] : 0LL, t[6] ? " <- last" : "");
-      }
-      for (int b = 0; b < 64; ++b) {
-        const long long* t = h + 64 * 8 + b * 8 + 8 * 64;
-        if (t[0] && t[5]) fprintf(f, "finish(cta %d): head %lld fold %lld divide %lld empties %lld check+prep %lld\n", b,
-                                  t[1] - t[0], t[2] - t[1], t[3] - t[2], t[4] - t[3], t[5] - t[4]);
-      }
-      for (int b = 0; b < 8; ++b) {
-        const long long* r = h + 2048 + b * 8;
-        const long long* t = h + 64 * 8 + b * 8;
-        if (r[0]) fprintf(f, "recheck cta %d: staged %lld  xload %lld  compute %lld  rest %lld  end->sync %lld\n", b,
-                          r[0] - t[1], r[1] - r[0], r[2] - r[1], r[3] - r[2], t[2] - r[3]);
-      }
-      {
-        long long e0 = 0, e1 = 0, m1 = 0, m0 = 0, t1 = 0, x1 = 0;
-        for (int b = 0; b < 1024; ++b) {
-          const long long* g = h + 4096 + b * 4;
-          if (!g[0]) break;
-          e0 = e0 ? std::min(e0, g[0]) : g[0]; e1 = std::max(e1, g[0]);
-          m0 = m0 ? std::min(m0, g[1]) : g[1]; m1 = std::max(m1, g[1]);
-          t1 = std::max(t1, g[2]); x1 = std::max(x1, g[3]);
-        }
-        fprintf(f, "gtimer(ns from first entry): last entry %lld  main end min %lld max %lld  tail end max %lld  exit max %lld\n",
-                e1 - e0, m0 - e0, m1 - e0, t1 - e0, x1 - e0);
       }
       fprintf(f, "----\n");
       fclose(f);
@@ -463,11 +443,12 @@ static void free_k(km_engine* e) {
   dfree(e->labels); dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
   dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->d2); dfree(e->partials); dfree(e->winner);
   dfree(e->scratch_d); dfree(e->labels64); dfree(e->wop); dfree(e->tot); dfree(e->recheck_rows);
-  dfree(e->recheck_count); dfree(e->cta_done);
+  dfree(e->recheck_count); dfree(e->cta_done); dfree(e->grid_sync);
   e->labels = nullptr; e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
   e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->d2 = nullptr; e->partials = nullptr; e->winner = nullptr;
   e->scratch_d = nullptr; e->labels64 = nullptr; e->wop = nullptr; e->tot = nullptr;
-  e->recheck_rows = nullptr; e->recheck_count = nullptr; e->cta_done = nullptr;
+  e->recheck_rows = nullptr; e->recheck_count = nullptr; e->cta_done = nullptr; e->grid_sync = nullptr;
+  e->resident_unfit = false;
   e->k = 0;
   e->kp = 0;
 }
@@ -500,6 +481,7 @@ static int ensure_k(km_engine* e, int32_t k) {
   if ((r = dalloc(e, &e->recheck_count, 16))) return r;
   CK(cudaMemsetAsync(e->recheck_count, 0, 16, e->stream));
   if ((r = dalloc(e, &e->cta_done, 16))) return r;
+  if ((r = dalloc(e, &e->grid_sync, 16))) return r;
   CK(cudaMemsetAsync(e->cta_done, 0, 16, e->stream));
   CK(cudaMemsetAsync(e->tot, 0, 8 * ((size_t)k * m + k), e->stream));
   e->next_full = true;
@@ -915,6 +897,47 @@ int km_converged(km_engine* e, const double* prev, const double* next, int32_t k
   return KM_OK;
 }
 
+// Tensor-core resident loop: the whole Lloyd iteration runs inside one cooperative launch
+// (lloyd_pass_tc_kernel with a.resident); the host only steps in for empty-cluster repairs.
+static int lloyd_resident(km_engine* e) {
+  int r;
+  const size_t nacc = (size_t)e->k * e->m + e->k;
+  CK(cudaMemsetAsync(e->tot, 0, 8 * nacc, e->stream));  // the first (full) pass adds every point
+  bool full = true;
+  for (;;) {
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    if (e->profiling) {
+      while (e->ev.size() < 2) {
+        cudaEvent_t ev;
+        CK(cudaEventCreate(&ev));
+        e->ev.push_back(ev);
+      }
+      ev0 = e->ev[0];
+      ev1 = e->ev[1];
+      CK(cudaEventRecord(ev0, e->stream));
+    }
+    const int passes_before = e->st_host->passes;
+    if ((r = launch_tc(e, full, true, false, true))) return r;
+    if (e->profiling) CK(cudaEventRecord(ev1, e->stream));
+    if ((r = read_state(e))) return r;
+    const DevState s = *e->st_host;
+    if (e->profiling && s.passes > passes_before) {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, ev0, ev1));
+      e->stats.pass_ms_total += ms;
+      e->stats.pass_timed += s.passes - passes_before;
+    }
+    full = false;
+    e->next_full = false;
+    if (s.done) return KM_OK;
+    if (!s.need_host) return set_err(e, KM_ERR_INTERNAL, "resident Lloyd loop stopped without a decision");
+    if ((r = repair_local(e))) return r;
+    if ((r = launch_check(e))) return r;
+    if ((r = read_state(e))) return r;
+    if (e->st_host->done) return KM_OK;
+  }
+}
+
 int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, double tol, double* centers_out,
              int64_t* counts_out, int64_t* labels_out, int32_t* iterations_out, int32_t* converged_out) {
   if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
@@ -931,6 +954,17 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
   if ((r = launch_prep(e))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   e->next_full = true;  // the labels buffer does not hold L of this run yet
+  bool ran_resident = false;
+  if (use_tc(e) && !e->resident_unfit && !getenv("KM_NO_RESIDENT")) {
+    r = lloyd_resident(e);
+    if (r == KM_RESIDENT_UNFIT) {
+      e->resident_unfit = true;
+    } else if (r) {
+      return r;
+    } else {
+      ran_resident = true;
+    }
+  }
   // Tensor-core path: ONE launch per iteration — pass t + (last CTA) finish t+1.
   // SIMT path: finish and pass are separate launches.
   const bool fused = use_tc(e);
@@ -972,10 +1006,10 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
     return KM_OK;
   };
   // L0 = A(C0) (engine.py:328), fused with the sums U(L0) needs (and, fused, the first update).
-  if ((r = timed_pass())) return r;
+  if (!ran_resident && (r = timed_pass())) return r;
   int first = 1;
   int t_before = 0;
-  for (;;) {
+  while (!ran_resident) {
     for (int b = 0; b < batch; ++b) {
       if (!fused && (r = launch_finish(e, 0, !prev_full))) return r;
       if ((r = timed_pass())) return r;

@@ -17,6 +17,8 @@ struct DevState {
   unsigned long long rechecked;
   unsigned long long changed;   // labels that changed in incremental passes
   double tol;
+  int32_t passes;     // passes run by resident launches (statistics)
+  int32_t pad_;
 };
 
 #ifdef __CUDACC__

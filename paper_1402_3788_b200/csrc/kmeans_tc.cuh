@@ -73,9 +73,8 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 // Wait strategy (build-time tuning knob):
-//   KM_WAIT_MODE 0: mbarrier.try_wait (HW suspend, default time limit)
 //   KM_WAIT_MODE 1: mbarrier.test_wait polling
-//   KM_WAIT_MODE 2: mbarrier.try_wait with a short suspend-time hint
+//   otherwise     : mbarrier.try_wait with a short suspend-time hint (bounded)
 #ifndef KM_WAIT_MODE
 #define KM_WAIT_MODE 2
 #endif
@@ -92,30 +91,31 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(64)
+      : "memory");
+  return ok != 0;
+}
+// try_wait with a short suspend-time hint; bounded: a wait that cannot complete (a bug)
+// traps after ~8 s instead of hanging the device
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if KM_WAIT_MODE == 1
   while (!mbar_test(bar, parity)) {
   }
-#elif KM_WAIT_MODE == 2
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(64)
-      : "memory");
 #else
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
+  if (mbar_try(bar, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(bar, parity)) {
+    if (clock64() - t0 > (1ll << 34)) __trap();
+  }
 #endif
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
@@ -239,21 +239,112 @@ struct TcTmem {
 template <int MP, int KP>
 struct TcSmem {
   static constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
-  uint32_t raw_stride, off_raw = 0, off_a, off_w, off_acc, off_q, off_bar, total;
-  __host__ __device__ explicit TcSmem(int m) {
+  uint32_t raw_stride, off_raw = 0, off_a, off_w, off_acc, off_q, off_c, off_bar, total;
+  // kres = k for the resident loop (two fp64 centre sets stay in shared memory), else 0
+  __host__ __device__ TcSmem(int m, int kres) {
     // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
     raw_stride = ((uint32_t)kTile * m * 4 + 256 + 1023) & ~1023u;
     off_a = RS * raw_stride;                 // [AS][128 rows × 128 B]
-    off_w = off_a + AS * kTile * 128;          // [2KP rows × 128 B]
-    off_acc = off_w + 2 * KP * 128;                  // [KP·(MP+1) + KP] int64 Δ accumulators
-    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // [kQueueCap] int64 rows + counter
-    off_bar = off_q + kQueueCap * 8 + 1024;
-    total = off_bar + 1024 + 1024;                   // barriers + 1 KiB alignment slack
+    off_w = off_a + AS * kTile * 128;        // [2KP rows × 128 B]
+    off_acc = off_w + 2 * KP * 128;          // [KP·(MP+1) + KP] int64 Δ accumulators
+    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // [kQueueCap] int64 rows + counters
+    off_c = off_q + kQueueCap * 8 + 1024;    // [2][kres·m] fp64 centres (resident)
+    off_bar = off_c + ((uint32_t)(2 * kres * m * 8) + 1023) / 1024 * 1024;
+    total = off_bar + 1024 + 1024;           // barriers + 1 KiB alignment slack
   }
 };
 
+// Exact label of one point by one thread (overflow of the CTA's recheck queue; rare):
+// the reference recurrence (features ascending, no FMA, strict '<' → lowest index).
+static __device__ __noinline__ int exact_label_thread(const float* __restrict__ xr, int m, int k,
+                                               const double* __restrict__ C) {
+  double bd = 0.0;
+  int bl = -1;
+  for (int c = 0; c < k; ++c) {
+    double acc = 0.0;
+    for (int f = 0; f < m; ++f) {
+      const double d = __dsub_rn((double)__ldg(xr + f), C[(size_t)c * m + f]);
+      acc = __dadd_rn(acc, __dmul_rn(d, d));
+    }
+    if (bl < 0 || acc < bd) { bd = acc; bl = c; }
+  }
+  return bl;
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Spin until *p ≥ target (one thread).  Bounded: a grid that is not co-resident (or a
+// bug) traps with an error after ~4 s instead of hanging the device.
+__device__ __forceinline__ void grid_spin(const unsigned int* p, unsigned int target) {
+  const long long t0 = clock64();
+  while (ld_acquire_u32(p) < target) {
+    if (clock64() - t0 > (1ll << 33)) __trap();
+  }
+}
+
+// Per-CTA filter prep for the resident loop: ‖fl32(c)‖², max ‖fl32(c)‖ and the fp16 hi/lo
+// B operand written straight into the CTA's SW128 tile — the same values block_prep_filter
+// (kmeans_finish.cuh) writes to global memory for the launch-per-iteration path.
+__device__ __forceinline__ void cta_prep_operand(const double* __restrict__ C, int k, int m, int kp, float pre,
+                                                 unsigned char* s_w, float* s_cmax) {
+  __shared__ double s_cn2[128];
+  __shared__ float s_red[32];
+  float local_max = 0.f;
+  for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
+    double s = 0.0;
+    for (int f = 0; f < m; ++f) {
+      const double v = (double)__double2float_rn(C[(size_t)cc * m + f]);
+      s = __fma_rn(v, v, s);
+    }
+    s_cn2[cc] = s;
+    local_max = fmaxf(local_max, __double2float_ru(sqrt(s) * (1.0 + 1e-12)));
+  }
+  for (int o = 16; o > 0; o >>= 1) local_max = fmaxf(local_max, __shfl_xor_sync(0xffffffffu, local_max, o));
+  if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = local_max;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mx = 0.f;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, s_red[i]);
+    s_cmax[0] = mx;
+  }
+  const int hw = 8 * ((m + 1 + 7) / 8);
+  for (int i = threadIdx.x; i < kp * 64; i += blockDim.x) {
+    const int cc = i >> 6, col = i & 63;
+    const int f = col < hw ? col : col - hw;
+    float v = 0.f;
+    if (cc < k && col < 2 * hw) {
+      if (f < m) v = -2.0f * __double2float_rn(C[(size_t)cc * m + f]) * pre;
+      else if (f == m) v = __double2float_rn(s_cn2[cc] * (double)pre * (double)pre);
+    } else if (cc >= k && col < 2 * hw && f == m) {
+      v = 65504.f;
+    }
+    const __half h = __float2half_rn(v);
+    const __half l = __float2half_rn(v - __half2float(h));
+    const uint32_t off = sw128(0, col >> 3) + (col & 7) * 2;
+    *reinterpret_cast<unsigned short*>(s_w + sw128(cc, col >> 3) + (col & 7) * 2) =
+        (col < 2 * hw) ? __half_as_ushort(h) : (unsigned short)0;
+    *reinterpret_cast<unsigned short*>(s_w + sw128(kp + cc, col >> 3) + (col & 7) * 2) =
+        (col < hw) ? __half_as_ushort(l) : (unsigned short)0;
+    (void)off;
+  }
+  fence_proxy_async();  // generic-proxy writes of the B tile → visible to the tensor core
+  __syncthreads();
+}
+
 // MT > 0: exact feature count m = MT (compile-time); MT < 0: runtime m ≤ −MT.
 // PRE: multiply x by the power-of-two prescale (off when the data range is fp16-safe as is).
+//
+// a.resident == 0: one pass (+ the finish in the last CTA to arrive when a.fuse_finish).
+// a.resident == 1: the Lloyd loop runs inside ONE cooperative launch (single GPU):
+//   pass t → flush the CTA's Δ into the running totals → grid barrier → every CTA
+//   computes C_{t+1} = S/N, the empty count, the congruence test and its own copy of
+//   the B operand (bit-identical in every CTA) → pass t+1.  The TMA producer streams
+//   the first tiles of pass t+1 while the tail, the barrier and the finish run.  Stops
+//   on convergence, after the final assign pass of an exhausted run, or on empty
+//   clusters (the host repairs them and relaunches).
 template <int MT, int KP, bool PRE>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
   static_assert(kThreadsTC == 576, "warp-role layout");
@@ -261,7 +352,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   if (a.gate && (a.st->done || a.st->need_host)) return;
   using L = TcLayout<MP>;
   using TM = TcTmem<KP>;
-  const TcSmem<MP, KP> S(MT > 0 ? MT : a.m);
+  const bool resident = a.resident != 0;
+  const TcSmem<MP, KP> S(MT > 0 ? MT : a.m, resident ? a.k : 0);
   constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1 KiB align the carve-up (SW128 atoms must be 1 KiB aligned); pointer arithmetic on the
@@ -271,26 +363,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   unsigned char* s_w = sm + S.off_w;
   unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(sm + S.off_acc);
   long long* s_q = reinterpret_cast<long long*>(sm + S.off_q);
-  unsigned int* s_qn = reinterpret_cast<unsigned int*>(sm + S.off_q + kQueueCap * 8);  // [0] count, [1] global base
+  unsigned int* s_qn = reinterpret_cast<unsigned int*>(sm + S.off_q + kQueueCap * 8);  // [0] queue length
+  float* s_cmax = reinterpret_cast<float*>(s_qn + 4);                                  // resident: max ‖c‖
+  double* s_cbuf = reinterpret_cast<double*>(sm + S.off_c);                            // resident: [2][k·m]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S.off_bar);
-  uint64_t* full_raw = bars;                        // [RS] TMA → transform
-  uint64_t* empty_raw = full_raw + RS;      // [RS] transform → TMA
-  uint64_t* a_full = empty_raw + RS;        // [AS]   transform → MMA
-  uint64_t* a_empty = a_full + AS;            // [AS]   MMA commit → transform
-  uint64_t* s_full = a_empty + AS;            // [NS]         MMA commit → epilogue
-  uint64_t* s_empty = s_full + TM::NS;              // [NS]         epilogue → MMA
+  uint64_t* full_raw = bars;                 // [RS] TMA → transform
+  uint64_t* empty_raw = full_raw + RS;       // [RS] transform → TMA
+  uint64_t* a_full = empty_raw + RS;         // [AS] transform → MMA
+  uint64_t* a_empty = a_full + AS;           // [AS] MMA commit → transform
+  uint64_t* s_full = a_empty + AS;           // [NS] MMA commit → epilogue
+  uint64_t* s_empty = s_full + TM::NS;       // [NS] epilogue → MMA
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(s_empty + TM::NS);
 
   const int m = MT > 0 ? MT : a.m;
   const int k = a.k;
+  const int km = k * m;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
-  const int nacc = k * m + k;
-  if (a.dbg_times != nullptr && tid == 0) {
-    a.dbg_times[64 * 8 + (blockIdx.x % 64) * 8 + 7] = clock64();
-    a.dbg_times[4096 + blockIdx.x * 4] = (long long)globaltimer();
-  }
+  const int nacc = km + k;
+  const int npre = resident ? min(RS, my_tiles) : 0;  // next-pass tiles streamed during the tail
 
   // ---- setup ----
   if (tid == 0) {
@@ -320,7 +412,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     for (int i = tid; i < AS * kTile * 8; i += nthr)
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
-    if (tid == 0) s_qn[0] = 0u;
+    if (resident)
+      for (int i = tid; i < km; i += nthr) s_cbuf[i] = a.c64[i];
+    if (tid == 0) {
+      s_qn[0] = 0u;
+      s_cmax[0] = a.cmax[0];
+    }
     fence_proxy_async();
   }
   tc_fence_before();
@@ -329,327 +426,431 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   const uint32_t tmem = *tmem_holder;
   const float pre = a.pre;
 
-  if (warp == kProducerWarp) {
-    // ===================== TMA producer: tile i → raw slot i % RS =====================
-    if (lane == 0) {
-      for (int i = 0; i < my_tiles; ++i) {
-        const int s = i % RS;
-        const int u = i / RS;
-        if (u > 0) mbar_wait(empty_raw + s, (u - 1) & 1);
-        const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
-        const int64_t row0 = t * kTile;
+  // loop state: every CTA derives the same decisions from the same totals
+  DevState* st = a.st;
+  int t_upd = st->t;
+  bool exhausted = st->exhausted != 0;
+  const int max_iters = st->max_iters;
+  const double tol = st->tol;
+  bool full = a.full != 0;
+  int cb = 0;      // resident: s_cbuf half holding C_t
+  int g0 = 0;      // tiles of earlier passes (ring positions continue across passes)
+  int issued = 0;  // producer: tiles of the current pass already in flight
+
+  for (int it = 0;; ++it) {
+    const double* C = resident ? s_cbuf + cb * km : a.c64;
+    if (warp == kProducerWarp) {
+      // ===================== TMA producer: tile g → raw slot g % RS =====================
+      if (lane == 0) {
+        auto issue = [&](int g, int i) {
+          const int s = g % RS;
+          if (g >= RS) mbar_wait(empty_raw + s, ((g / RS) - 1) & 1);
+          const int64_t row0 = (blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+          const int64_t rem = a.n - row0;
+          const int rows = rem < kTile ? (int)rem : kTile;
+          const uint32_t bytes = ((uint32_t)rows * m * 4u) & ~15u;
+          mbar_arrive_expect_tx(full_raw + s, bytes);
+          if (bytes)
+            bulk_g2s(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes, full_raw + s);
+        };
+        for (int i = issued; i < my_tiles; ++i) issue(g0 + i, i);
+        for (int j = 0; j < npre; ++j) issue(g0 + my_tiles + j, j);  // next pass (resident)
+      }
+      issued = npre;
+    } else if (warp == kMmaWarp) {
+      // ===================== MMA issuer (one thread) =====================
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(sm + S.off_a), w0 = smem_u32(s_w);
+        constexpr uint32_t idesc = idesc_f16(2 * KP);
+        for (int i = 0; i < my_tiles; ++i) {
+          const int g = g0 + i;
+          const int sa = g % AS, ss = g % TM::NS;
+          mbar_wait(a_full + sa, (g / AS) & 1);
+          if (g >= TM::NS) mbar_wait(s_empty + ss, ((g / TM::NS) - 1) & 1);
+          tc_fence_after();
+          const uint32_t ag = a0 + sa * (kTile * 128);
+          const uint32_t dcol = tmem + ss * 2 * KP;
+#pragma unroll
+          for (int ks = 0; ks < L::KSTEPS; ++ks) {
+            if (a.dbg_flags & 2) break;
+            mma_f16(dcol, make_desc(ag + ks * 32, 16, 1024), make_desc(w0 + ks * 32, 16, 1024), idesc,
+                    ks > 0 ? 1u : 0u);
+          }
+          mma_commit(s_full + ss);   // scores ready
+          mma_commit(a_empty + sa);  // A buffer consumed
+        }
+      }
+    } else if (warp < kTransformWarps) {
+      // ===================== transform: thread = point; group tg takes tiles g ≡ tg (mod 2) =====================
+      const int tg = warp >> 2;
+      const int p = tid & 127;
+      const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
+      const int key = p & 7;
+      const float* __restrict__ gx = a.x;
+      for (int i = (tg - (g0 & 1)) & 1; i < my_tiles; i += kTransformGroups) {
+        const int g = g0 + i;
+        const int s = g % RS, sa = g % AS;
+        const int64_t row0 = (blockIdx.x + (int64_t)i * gridDim.x) * kTile;
         const int64_t rem = a.n - row0;
         const int rows = rem < kTile ? (int)rem : kTile;
-        const uint32_t bytes = ((uint32_t)rows * m * 4u) & ~15u;
-        mbar_arrive_expect_tx(full_raw + s, bytes);
-        if (bytes) bulk_g2s(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes,
-                            full_raw + s);
+        const bool active = p < rows;
+        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && g < 64;
+        long long* ts = stamp ? a.dbg_times + (size_t)g * 8 : nullptr;
+        if (stamp) ts[0] = clock64();
+        mbar_wait(full_raw + s, (g / RS) & 1);
+        if (stamp) ts[1] = clock64();
+        const float* rs = raw + s * (S.raw_stride / 4);
+        float xs[L::HW];
+        if (rows == kTile) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
+          const float* xr = rs + p * m;
+#pragma unroll
+          for (int f = 0; f < L::HW; ++f) {
+            const float v = (f < MP) ? xr[f] : 0.f;
+            xs[f] = (f < m) ? (PRE ? v * pre : v) : 0.f;
+          }
+        } else {  // ragged last tile: bulk part + ≤ 3 trailing floats from global
+          const uint32_t bulk_elems = (((uint32_t)rows * m * 4u) & ~15u) >> 2;
+          for (int f = 0; f < L::HW; ++f) {
+            float v = 0.f;
+            if (f < MP && f < m && active) {
+              const uint32_t e = (uint32_t)p * m + f;
+              v = ((e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e));
+              if (PRE) v *= pre;
+            }
+            xs[f] = v;
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < L::HW; ++f)
+          if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
+        uint32_t hw[L::HW / 2], lw[L::HW / 2];
+#pragma unroll
+        for (int q = 0; q < L::HW / 2; ++q) {
+          const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
+          const float2 hf = __half22float2(h2);
+          const __half2 l2 = __floats2half2_rn(xs[2 * q] - hf.x, xs[2 * q + 1] - hf.y);
+          hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
+          lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
+        }
+        // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
+        // the TMA producer may refill it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty_raw + s);
+        if (stamp) ts[7] = clock64();
+        if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);
+        if (stamp) ts[2] = clock64();
+        unsigned char* s_a = sm + S.off_a + sa * (kTile * 128);
+#pragma unroll
+        for (int q = 0; q < L::HW / 8; ++q) {
+          *reinterpret_cast<uint4*>(s_a + row_off + ((uint32_t)(q ^ key) << 4)) =
+              make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+          *reinterpret_cast<uint4*>(s_a + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
+              make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + sa);
+        if (stamp) ts[3] = clock64();
       }
-    }
-  } else if (warp == kMmaWarp) {
-    // ===================== MMA issuer (one thread) =====================
-    if (lane == 0) {
-      const uint32_t a0 = smem_u32(sm + S.off_a), w0 = smem_u32(s_w);
-      constexpr uint32_t idesc = idesc_f16(2 * KP);
-      for (int i = 0; i < my_tiles; ++i) {
-        const int sa = i % AS, ss = i % TM::NS;
-        mbar_wait(a_full + sa, (i / AS) & 1);
-        if (i >= TM::NS) mbar_wait(s_empty + ss, ((i / TM::NS) - 1) & 1);
+    } else {
+      // ===================== epilogue groups: thread = point = TMEM lane; group e takes tiles g ≡ e (mod 2) =====================
+      const int ew = warp - kTransformWarps;  // 0..7
+      const int e = ew >> 2;
+      const int p = ((ew & 3) << 5) | lane;  // TMEM lane of this thread
+      const uint32_t lane_base = (uint32_t)((ew & 3) * 32) << 16;
+      const float scale_f = a.scale_f;
+      // certified bound with the dataset's max ‖x‖ (per pass constant, prescaled units)
+      const float tt = (a.xnorm_max + (resident ? s_cmax[0] : a.cmax[0])) * pre;
+      const float E2 = 2.f * __fmaf_rn(a.err_coef * tt, tt, a.err_floor);
+      const float inv_pre2 = 1.0f / (pre * pre);
+      const double scale_d = a.scale_d;
+      const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0;
+      unsigned int my_changed = 0;
+      auto prev_label = [&](int i) -> int {  // previous label of this thread's point in tile i (or -1)
+        if (full || i >= my_tiles) return -1;
+        const int64_t r = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + p;
+        return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
+      };
+      const int i0 = (e - (g0 & 1)) & 1;
+      int old_next = prev_label(i0);
+      for (int i = i0; i < my_tiles; i += kEpiGroups) {
+        const int g = g0 + i;
+        const int ss = g % TM::NS;
+        const int64_t row0 = (blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+        const int64_t rem = a.n - row0;
+        const int rows = rem < kTile ? (int)rem : kTile;
+        const bool active = p < rows;
+        const int old = old_next;
+        old_next = prev_label(i + kEpiGroups);  // prefetch one tile ahead (global latency off the critical path)
+        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && g < 64;
+        long long* ts = stamp ? a.dbg_times + (size_t)g * 8 : nullptr;
+        if (stamp) ts[4] = clock64();
+        mbar_wait(s_full + ss, (g / TM::NS) & 1);
+        if (stamp) ts[5] = clock64();
         tc_fence_after();
-        const uint32_t ag = a0 + sa * (kTile * 128);
-        const uint32_t dcol = tmem + ss * 2 * KP;
+        // top-2 over the scores: per 16-column chunk a 4-level tree, then a running merge.
+        // (The filter's argmin tie order is irrelevant: a tie is never certified.)
+        float best = __int_as_float(0x7f800000), min2 = best;
+        int bi = 0;
 #pragma unroll
-        for (int ks = 0; ks < L::KSTEPS; ++ks) {
-          if (a.dbg_flags & 2) break;
-          mma_f16(dcol, make_desc(ag + ks * 32, 16, 1024), make_desc(w0 + ks * 32, 16, 1024), idesc,
-                  ks > 0 ? 1u : 0u);
-        }
-        mma_commit(s_full + ss);   // scores ready
-        mma_commit(a_empty + sa);  // A buffer consumed
-      }
-    }
-  } else if (warp < kTransformWarps) {
-    // ===================== transform: thread = point; group tg takes tiles i ≡ tg (mod 2) =====================
-    const int tg = warp >> 2;
-    const int p = tid & 127;
-    const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
-    const int key = p & 7;
-    const float* __restrict__ gx = a.x;
-    for (int i = tg; i < my_tiles; i += kTransformGroups) {
-      const int s = i % RS, sa = i % AS;
-      const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
-      const int64_t row0 = t * kTile;
-      const int64_t rem = a.n - row0;
-      const int rows = rem < kTile ? (int)rem : kTile;
-      const bool active = p < rows;
-      const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64;
-      long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
-      if (stamp) ts[0] = clock64();
-      mbar_wait(full_raw + s, (i / RS) & 1);
-      if (stamp) ts[1] = clock64();
-      const float* rs = raw + s * (S.raw_stride / 4);
-      float xs[L::HW];
-      if (rows == kTile) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
-        const float* xr = rs + p * m;
+        for (int c0 = 0; c0 < KP; c0 += 16) {
+          uint32_t r0[16], r1[16];
+          tmem_ld16(tmem + lane_base + ss * 2 * KP + c0, r0);
+          tmem_ld16(tmem + lane_base + ss * 2 * KP + KP + c0, r1);
+          tmem_ld_wait();
+          float v[16], s2[16];
+          int ix[16];
 #pragma unroll
-        for (int f = 0; f < L::HW; ++f) {
-          const float v = (f < MP) ? xr[f] : 0.f;
-          xs[f] = (f < m) ? (PRE ? v * pre : v) : 0.f;
-        }
-      } else {              // ragged last tile: bulk part + ≤ 3 trailing floats from global
-        const uint32_t bulk_elems = (((uint32_t)rows * m * 4u) & ~15u) >> 2;
-        for (int f = 0; f < L::HW; ++f) {
-          float v = 0.f;
-          if (f < MP && f < m && active) {
-            const uint32_t e = (uint32_t)p * m + f;
-            v = ((e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e));
-            if (PRE) v *= pre;
+          for (int jj = 0; jj < 16; ++jj) {  // padded centres (c ≥ k) score +65504: never best or runner-up
+            v[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+            s2[jj] = __int_as_float(0x7f800000);
+            ix[jj] = c0 + jj;
           }
-          xs[f] = v;
+          if (a.dbg_scores != nullptr && active) {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              if (c0 + jj < k) a.dbg_scores[(row0 + p) * k + c0 + jj] = v[jj] * inv_pre2;
+          }
+#pragma unroll
+          for (int w = 1; w < 16; w <<= 1) {
+#pragma unroll
+            for (int jj = 0; jj < 16; jj += 2 * w) {
+              const bool rb = v[jj + w] < v[jj];
+              const float lo = rb ? v[jj + w] : v[jj], hi = rb ? v[jj] : v[jj + w];
+              s2[jj] = fminf(hi, fminf(s2[jj], s2[jj + w]));
+              ix[jj] = rb ? ix[jj + w] : ix[jj];
+              v[jj] = lo;
+            }
+          }
+          const bool rb = v[0] < best;
+          min2 = fminf(rb ? best : v[0], fminf(min2, s2[0]));
+          bi = rb ? ix[0] : bi;
+          best = rb ? v[0] : best;
         }
-      }
-#pragma unroll
-      for (int f = 0; f < L::HW; ++f)
-        if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
-      uint32_t hw[L::HW / 2], lw[L::HW / 2];
-#pragma unroll
-      for (int q = 0; q < L::HW / 2; ++q) {
-        const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
-        const float2 hf = __half22float2(h2);
-        const __half2 l2 = __floats2half2_rn(xs[2 * q] - hf.x, xs[2 * q + 1] - hf.y);
-        hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
-        lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
-      }
-      // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
-      // the TMA producer may refill it
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_raw + s);
-      if (stamp) ts[7] = clock64();
-      if (i >= AS) mbar_wait(a_empty + sa, ((i / AS) - 1) & 1);
-      if (stamp) ts[2] = clock64();
-      unsigned char* s_a = sm + S.off_a + sa * (kTile * 128);
-#pragma unroll
-      for (int q = 0; q < L::HW / 8; ++q) {
-        *reinterpret_cast<uint4*>(s_a + row_off + ((uint32_t)(q ^ key) << 4)) =
-            make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-        *reinterpret_cast<uint4*>(s_a + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
-            make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
-      }
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_full + sa);
-      if (stamp) ts[3] = clock64();
-    }
-  } else {
-    // ===================== epilogue groups: thread = point = TMEM lane; group e takes tiles i ≡ e (mod 2) =====================
-    const int ew = warp - kTransformWarps;          // 0..7
-    const int e = ew >> 2;
-    const int p = ((ew & 3) << 5) | lane;          // TMEM lane of this thread
-    const uint32_t lane_base = (uint32_t)((ew & 3) * 32) << 16;
-    const float scale_f = a.scale_f;
-    // certified bound with the dataset's max ‖x‖ (per launch constant, prescaled units)
-    const float tt = (a.xnorm_max + a.cmax[0]) * pre;
-    const float E2 = 2.f * __fmaf_rn(a.err_coef * tt, tt, a.err_floor);
-    const float inv_pre2 = 1.0f / (pre * pre);
-    const double scale_d = a.scale_d;
-    const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0, full = a.full != 0;
-    unsigned int my_changed = 0;
-    auto prev_label = [&](int i) -> int {  // previous label of this thread's point in tile i (or -1)
-      if (full || i >= my_tiles) return -1;
-      const int64_t r = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + p;
-      return r < a.n ? __ldg(a.labels + r) : -1;
-    };
-    int old_next = prev_label(e);
-    for (int i = e; i < my_tiles; i += kEpiGroups) {
-      const int ss = i % TM::NS;
-      const int64_t t = blockIdx.x + (int64_t)i * gridDim.x;
-      const int64_t row0 = t * kTile;
-      const int64_t rem = a.n - row0;
-      const int rows = rem < kTile ? (int)rem : kTile;
-      const bool active = p < rows;
-      const int old = old_next;
-      old_next = prev_label(i + kEpiGroups);  // prefetch one tile ahead (global latency off the critical path)
-      const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64;
-      long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
-      if (stamp) ts[4] = clock64();
-      mbar_wait(s_full + ss, (i / TM::NS) & 1);
-      if (stamp) ts[5] = clock64();
-      tc_fence_after();
-      // top-2 over the scores: per 16-column chunk a 4-level tree, then a running merge.
-      // (The filter's argmin tie order is irrelevant: a tie is never certified.)
-      float best = __int_as_float(0x7f800000), min2 = best;
-      int bi = 0;
-#pragma unroll
-      for (int c0 = 0; c0 < KP; c0 += 16) {
-        uint32_t r0[16], r1[16];
-        tmem_ld16(tmem + lane_base + ss * 2 * KP + c0, r0);
-        tmem_ld16(tmem + lane_base + ss * 2 * KP + KP + c0, r1);
-        tmem_ld_wait();
-        float v[16], s2[16];
-        int ix[16];
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {  // padded centres (c ≥ k) score +65504: never best or runner-up
-          v[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
-          s2[jj] = __int_as_float(0x7f800000);
-          ix[jj] = c0 + jj;
-        }
-        if (a.dbg_scores != nullptr && active) {
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj)
-            if (c0 + jj < k) a.dbg_scores[(row0 + p) * k + c0 + jj] = v[jj] * inv_pre2;
-        }
-#pragma unroll
-        for (int w = 1; w < 16; w <<= 1) {
-#pragma unroll
-          for (int jj = 0; jj < 16; jj += 2 * w) {
-            const bool rb = v[jj + w] < v[jj];
-            const float lo = rb ? v[jj + w] : v[jj], hi = rb ? v[jj] : v[jj + w];
-            s2[jj] = fminf(hi, fminf(s2[jj], s2[jj + w]));
-            ix[jj] = rb ? ix[jj + w] : ix[jj];
-            v[jj] = lo;
+        tc_fence_before();  // TMEM reads ordered before the MMA reuses this buffer
+        __syncwarp();
+        if (lane == 0) mbar_arrive(s_empty + ss);
+        const bool certified = !exact_only && (min2 > best + E2);
+        bool apply = active && certified && bi != old;
+        if (active && !certified) {
+          // defer to the CTA's tail (warp-cooperative exact re-decision)
+          const unsigned int slot = atomicAdd(s_qn, 1u);
+          if (slot < kQueueCap) {
+            s_q[slot] = ((row0 + p) << 24) | (long long)(old + 1);  // row | previous label (+1; 0 = none)
+          } else {  // staging full (rare): decide it here, thread-serial
+            bi = exact_label_thread(a.x + (row0 + p) * m, m, k, C);
+            apply = bi != old;
           }
         }
-        const bool rb = v[0] < best;
-        min2 = fminf(rb ? best : v[0], fminf(min2, s2[0]));
-        bi = rb ? ix[0] : bi;
-        best = rb ? v[0] : best;
-      }
-      tc_fence_before();  // TMEM reads ordered before the MMA reuses this buffer
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty + ss);
-      const bool certified = !exact_only && (min2 > best + E2);
-      if (active && !certified) {
-        // defer: recheck_kernel re-decides this point exactly and applies its update
-        const unsigned int slot = atomicAdd(s_qn, 1u);
-        if (slot < kQueueCap) {
-          s_q[slot] = ((row0 + p) << 24) | (long long)(old + 1);  // row | previous label (+1; 0 = none)
-        } else {  // CTA staging full: straight to the global queue
-          a.recheck_rows[atomicAdd(a.recheck_count, 1u)] = row0 + p;
+        if (apply) {
+          // --- exact incremental update of the per-cluster fixed-point sums
+          ++my_changed;
+          a.labels[row0 + p] = bi;
+          const float* xr = a.x + (row0 + p) * m;  // just streamed: L2 hit
+          for (int f = 0; f < m; ++f) {
+            const float xv = __ldg(xr + f);
+            const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d))
+                                           : __float2ll_rn(__fmul_rn(xv, scale_f));
+            smem_add64(s_acc + (size_t)bi * m + f, (unsigned long long)v);
+            if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
+          }
+          smem_add64(s_acc + (size_t)km + bi, 1ull);
+          if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
         }
-      } else if (active && bi != old) {
-        // --- exact incremental update of the per-cluster fixed-point sums
-        ++my_changed;
-        a.labels[row0 + p] = bi;
-        const float* xr = a.x + (row0 + p) * m;  // just streamed: L2 hit
-        for (int f = 0; f < m; ++f) {
-          const float xv = __ldg(xr + f);
-          const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d))
-                                         : __float2ll_rn(__fmul_rn(xv, scale_f));
-          smem_add64(s_acc + (size_t)bi * m + f, (unsigned long long)v);
-          if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
-        }
-        smem_add64(s_acc + (size_t)k * m + bi, 1ull);
-        if (old >= 0) smem_add64(s_acc + (size_t)k * m + old, ~0ull);
+        if (stamp) ts[6] = clock64();
       }
-      if (stamp) ts[6] = clock64();
-    }
-    unsigned int w2 = my_changed;
+      if (!full) {
+        unsigned int w2 = my_changed;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) w2 += __shfl_xor_sync(0xffffffffu, w2, o);
-    if (lane == 0 && w2) atomicAdd(&a.st->changed, (unsigned long long)w2);
+        for (int o = 16; o > 0; o >>= 1) w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+        if (lane == 0 && w2) atomicAdd(&st->changed, (unsigned long long)w2);
+      }
+    }
+    // ===================== tail (all warps) =====================
+    tc_fence_before();
+    __syncthreads();  // every role done with this pass: Δ atomics and the CTA's recheck queue are complete
+    const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
+    const double* Cx = C;  // fp64 centres of the pass for the exact re-decision
+    double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
+    const int stage_cap = (int)(RS * S.raw_stride / 8);
+    if (!resident && qn && km <= stage_cap) {
+      // the raw ring is idle now (no next-pass prefetch): stage the fp64 centres there
+      for (int i = tid; i < km; i += kThreadsTC) s_stage[i] = a.c64[i];
+      __syncthreads();
+      Cx = s_stage;
+    }
+    {
+      // exact re-decision of this CTA's uncertified points, 4 per warp (x rows fetched together), Δ into s_acc
+      for (unsigned int q0 = warp * 4; q0 < qn; q0 += (kThreadsTC / 32) * 4) {
+        long long ent[4];
+        float xb[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          ent[j] = (q0 + j < qn) ? s_q[q0 + j] : -1;
+          xb[j] = (ent[j] >= 0 && lane < m) ? __ldg(a.x + (ent[j] >> 24) * m + lane) : 0.f;
+        }
+        int lb[4];
+        exact_label_warp_batch<MP, 4>(xb, m, k, Cx, lb);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (ent[j] < 0) continue;
+          const long long row = ent[j] >> 24;
+          const float xl = xb[j];
+          const int bl = lb[j];
+          const int old = full ? -1 : (int)(ent[j] & 0xffffff) - 1;
+          if (bl != old) {
+            if (lane == 0) {
+              a.labels[row] = bl;
+              smem_add64(s_acc + (size_t)km + bl, 1ull);
+              if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+              if (!full) atomicAdd(&st->changed, 1ull);
+            }
+            if (lane < m) {
+              const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xl, a.scale_d))
+                                               : __float2ll_rn(__fmul_rn(xl, a.scale_f));
+              smem_add64(s_acc + (size_t)bl * m + lane, (unsigned long long)v);
+              if (old >= 0) smem_add64(s_acc + (size_t)old * m + lane, (unsigned long long)(-v));
+            }
+          }
+        }
+      }
+      if (tid == 0 && s_qn[0]) atomicAdd(&st->rechecked, (unsigned long long)s_qn[0]);
+    }
+    __syncthreads();
+    if (!resident) {
+      for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
+        const unsigned long long v = s_acc[i];
+        if (v) atomicAdd(a.part + i, v);
+      }
+      if (a.fuse_finish) {
+        // the last CTA to arrive runs the finish of this iteration (no separate launch)
+        __shared__ int s_last;
+        __threadfence();
+        __syncthreads();
+        if (tid == 0) s_last = atomicAdd(a.cta_done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (s_last) {
+          __threadfence();
+          finish_block(a.fin, s_stage, stage_cap);
+          if (tid == 0) *a.cta_done = 0u;
+        }
+      }
+      break;
+    }
+    // ---- resident: Δ → running totals, grid barrier ----
+    // the totals of the previous pass must have been read by every CTA before they move again
+    if (tid == 0) grid_spin(a.grid_sync + 1, (unsigned int)it * gridDim.x);
+    __syncthreads();
+    unsigned long long* tot = a.fin.tot;
+    for (int i = tid; i < nacc; i += kThreadsTC) {
+      const unsigned long long v = s_acc[i];
+      if (v) atomicAdd(tot + i, v);
+      s_acc[i] = 0ull;
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      s_qn[0] = 0u;
+      atomicAdd(a.grid_sync, 1u);
+      grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
+    }
+    __syncthreads();
+    // ---- resident finish (every CTA; CTA 0 publishes) — engine._finish_update / converged ----
+    const bool pub = blockIdx.x == 0;
+    bool stop = false;
+    if (pub && tid == 0) st->passes += 1;
+    if (exhausted) {
+      // the final assign pass of an exhausted run: counts = bincount(L_T), C_T unchanged
+      if (pub) {
+        for (int cc = tid; cc < k; cc += kThreadsTC) a.fin.model_counts[cc] = (long long)__ldcg(tot + km + cc);
+        if (tid == 0) st->done = 1;
+      }
+      stop = true;
+    } else {
+      double* Cn = s_cbuf + (cb ^ 1) * km;
+      for (int i = tid; i < km; i += kThreadsTC) {
+        const long long nc = (long long)__ldcg(tot + km + i / m);
+        const long long sv = (long long)__ldcg(tot + i);
+        // empty clusters get a placeholder; every one is re-seeded by the host repair
+        Cn[i] = nc > 0 ? __ddiv_rn(__dmul_rn((double)sv, a.fin.inv_scale), (double)nc) : 0.0;
+      }
+      long long nc_mine = 0;
+      if (tid < k) nc_mine = (long long)__ldcg(tot + km + tid);
+      const int n_empty = __syncthreads_count(tid < k && nc_mine == 0);  // also: Cn complete
+      if (tid == 0) {  // this CTA is done reading the totals
+        __threadfence();
+        atomicAdd(a.grid_sync + 1, 1u);
+      }
+      ++t_upd;
+      if (pub) {
+        for (int i = tid; i < km; i += kThreadsTC) {
+          a.fin.prev[i] = C[i];
+          a.fin.cur[i] = Cn[i];
+        }
+        if (tid < k) a.fin.model_counts[tid] = nc_mine;
+        if (tid == 0) {
+          st->t = t_upd;
+          st->n_empty = n_empty;
+        }
+      }
+      if (n_empty > 0) {
+        if (pub && tid == 0) st->need_host = 1;
+        stop = true;
+      } else {
+        __shared__ double s_redd[32];
+        const int conv = block_converged(C, Cn, k, m, tol, s_redd);
+        if (conv) {
+          if (pub && tid == 0) {
+            st->converged = 1;
+            st->done = 1;
+          }
+          stop = true;
+        } else {
+          if (t_upd >= max_iters) {  // reference: one more assign pass, then return
+            exhausted = true;
+            if (pub && tid == 0) st->exhausted = 1;
+          }
+          cta_prep_operand(Cn, k, m, KP, pre, s_w, s_cmax);
+          cb ^= 1;
+          full = false;
+        }
+      }
+    }
+    __syncthreads();
+    if (stop) break;
+    g0 += my_tiles;
   }
-  // ===================== tail (all warps) =====================
-  long long* tstamp = (a.dbg_times != nullptr && tid == 0) ? a.dbg_times + 64 * 8 + (blockIdx.x % 64) * 8 : nullptr;
-  if (tstamp) tstamp[0] = clock64();
-  if (a.dbg_times != nullptr && tid == 0) a.dbg_times[4096 + blockIdx.x * 4 + 1] = (long long)globaltimer();
+  // ---- teardown ----
+  if (resident && warp == kProducerWarp && lane == 0) {
+    // the prefetched tiles of the pass that does not run: let their copies land before exit
+    for (int j = 0; j < npre; ++j) {
+      const int g = g0 + my_tiles + j;
+      mbar_wait(full_raw + g % RS, (g / RS) & 1);
+    }
+  }
   tc_fence_before();
-  __syncthreads();  // every role done: Δ atomics and the CTA's recheck queue are complete
-  if (tstamp) tstamp[1] = clock64();
+  __syncthreads();
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, TM::alloc);
   }
-  // the raw ring is free now: stage the fp64 centres there for the recheck (and the finish)
-  double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
-  const int stage_cap = (int)(RS * S.raw_stride / 8);
-  const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
-  const bool c_staged = k * m <= stage_cap;
-  if (qn && c_staged) {
-    for (int i = tid; i < k * m; i += kThreadsTC) s_stage[i] = a.c64[i];
-    __syncthreads();
-  }
-  long long* rst = (a.dbg_times != nullptr && lane == 0 && warp == 0) ? a.dbg_times + 2048 + (blockIdx.x % 64) * 8 : nullptr;
-  if (rst) rst[0] = clock64();
-  {
-    // exact re-decision of this CTA's uncertified points (warp per point), Δ into s_acc
-    const bool full = a.full != 0;
-    const double* C = c_staged ? s_stage : a.c64;
-    // batches of 4 points per warp: their x rows (one feature per lane) are fetched together
-    for (unsigned int q0 = warp * 4; q0 < qn; q0 += (kThreadsTC / 32) * 4) {
-      long long ent[4];
-      float xb[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        ent[j] = (q0 + j < qn) ? s_q[q0 + j] : -1;
-        xb[j] = (ent[j] >= 0 && lane < m) ? __ldg(a.x + (ent[j] >> 24) * m + lane) : 0.f;
-      }
-      if (rst && q0 == 0) { rst[1] = clock64() + (long long)(xb[0] + xb[1] + xb[2] + xb[3] == 12345.f); }
-      int lb[4];
-      exact_label_warp_batch<MP, 4>(xb, m, k, C, lb);
-      if (rst && q0 == 0) { rst[2] = clock64() + (lb[0] + lb[1] + lb[2] + lb[3] == 12345); }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        if (ent[j] < 0) continue;
-        const long long row = ent[j] >> 24;
-        const float xl = xb[j];
-        const int bl = lb[j];
-        const int old = full ? -1 : (int)(ent[j] & 0xffffff) - 1;
-        if (bl != old) {
-          if (lane == 0) {
-            a.labels[row] = bl;
-            smem_add64(s_acc + (size_t)k * m + bl, 1ull);
-            if (old >= 0) smem_add64(s_acc + (size_t)k * m + old, ~0ull);
-            if (!full) atomicAdd(&a.st->changed, 1ull);
-          }
-          if (lane < m) {
-            const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xl, a.scale_d))
-                                             : __float2ll_rn(__fmul_rn(xl, a.scale_f));
-            smem_add64(s_acc + (size_t)bl * m + lane, (unsigned long long)v);
-            if (old >= 0) smem_add64(s_acc + (size_t)old * m + lane, (unsigned long long)(-v));
-          }
-        }
-      }
-    }
-    if (rst) rst[3] = clock64();
-    if (tid == 0 && qn) atomicAdd(&a.st->rechecked, (unsigned long long)qn);
-    if (tstamp) tstamp[5] = qn;
-  }
-  __syncthreads();
-  if (tstamp) tstamp[2] = clock64();
-  if (a.dbg_times != nullptr && tid == 0) a.dbg_times[4096 + blockIdx.x * 4 + 2] = (long long)globaltimer();
-  for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
-    const unsigned long long v = s_acc[i];
-    if (v) atomicAdd(a.part + i, v);
-  }
-  if (a.fuse_finish) {
-    // the last CTA to arrive runs the finish of this iteration (no separate launch)
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) s_last = atomicAdd(a.cta_done, 1u) == gridDim.x - 1;
-    __syncthreads();
-    if (tstamp) tstamp[3] = clock64();
-    if (s_last) {
-      __threadfence();
-      finish_block(a.fin, s_stage, stage_cap, tstamp ? tstamp + 8 * 64 : nullptr);
-      if (tid == 0) *a.cta_done = 0u;
-      if (tstamp) { tstamp[4] = clock64(); tstamp[6] = 1; }
-    }
-  }
-  if (a.dbg_times != nullptr && tid == 0) a.dbg_times[4096 + blockIdx.x * 4 + 3] = (long long)globaltimer();
 }
 
 template <int MT, int KP, bool PRE>
 inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_t stream, cudaError_t* ce, char* msg,
-             size_t len) {
+                    size_t len) {
   auto kern = lloyd_pass_tc_kernel<MT, KP, PRE>;
   constexpr int MP = MT > 0 ? MT : -MT;
-  const size_t smem = TcSmem<MP, KP>(a.m).total;
-  if (smem > smem_optin) {
-    snprintf(msg, len, "tensor-core pass needs %zu B of shared memory (max %zu)", smem, smem_optin);
-    return 2;
+  cudaFuncAttributes fa{};
+  cudaError_t c = cudaFuncGetAttributes(&fa, kern);
+  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncGetAttributes(tc)"); return 1; }
+  const size_t smem = TcSmem<MP, KP>(a.m, a.resident ? a.k : 0).total;
+  if (smem + fa.sharedSizeBytes > smem_optin) {
+    snprintf(msg, len, "tensor-core pass needs %zu B of shared memory (max %zu)", smem + fa.sharedSizeBytes,
+             smem_optin);
+    return a.resident ? 3 : 2;
   }
-  cudaError_t c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc smem)"); return 1; }
   c = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc carveout)"); return 1; }
@@ -659,8 +860,17 @@ inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_
   if (per_sm < 1) { snprintf(msg, len, "tensor-core pass does not fit on an SM"); return 2; }
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));  // one persistent CTA/SM
-  kern<<<(unsigned)grid, kThreadsTC, smem, stream>>>(a);
-  c = cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(kThreadsTC);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // resident loop: grid barrier needs every CTA co-resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = a.resident ? 1 : 0;
+  c = cudaLaunchKernelEx(&cfg, kern, a);
   if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "lloyd_pass_tc_kernel launch"); return 1; }
   return 0;
 }

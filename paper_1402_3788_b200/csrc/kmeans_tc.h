@@ -38,6 +38,8 @@ struct TcArgs {
   int32_t fuse_finish;     // 1: the last CTA to finish runs finish_block(fin) (single-GPU loop)
   unsigned int* cta_done;  // completion counter for the fused finish (self-resetting)
   FinishArgs fin;
+  int32_t resident;        // 1: run the whole loop in this (cooperative) launch, see lloyd_pass_tc_kernel
+  unsigned int* grid_sync; // resident: [0] barrier arrivals, [1] totals consumed (zeroed before the launch)
   DevState* st;
   int32_t gate;
   float* dbg_scores;       // optional n × k raw tensor-core scores, unscaled (tests)
@@ -46,7 +48,8 @@ struct TcArgs {
 };
 
 // Launch lloyd_pass_tc_kernel<mp, kp>.  Returns 0 on success, 1 on a CUDA error
-// (*cuda_err set), 2 if the shape does not fit; msg receives a description.
+// (*cuda_err set), 2 if the shape does not fit, 3 if only the resident variant does not
+// fit (the launch-per-iteration variant may); msg receives a description.
 int launch(const TcArgs& a, int mp, int kp, int num_sms, size_t smem_optin, cudaStream_t stream,
            cudaError_t* cuda_err, char* msg, size_t msg_len);
 
