@@ -281,8 +281,31 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
       for (int i = 0; i < 64; ++i) {
         if (!h[i * 8]) continue;
         const long long* t = h + i * 8;  // transform: raw wait, compute, A-buffer wait, store; epilogue: s wait, body
-        fprintf(f, "tile %2d  T: raw %5lld comp %5lld awaitA %5lld sts %5lld | E: swait %5lld body %5lld | t0 %lld\n", i,
-                t[1] - t[0], t[7] - t[1], t[2] - t[7], t[3] - t[2], t[5] - t[4], t[6] - t[5], t[0] - h[0]);
+        const long long* u = h + 3072 + i * 4;
+        fprintf(f, "tile %2d  T: raw %5lld comp %5lld awaitA %5lld sts %5lld | E: swait %5lld body %5lld | t0 %lld"
+                "  | M: afull-wait %lld sempty-wait %lld issue %lld  loop %lld\n", i,
+                t[1] - t[0], t[7] - t[1], t[2] - t[7], t[3] - t[2], t[5] - t[4], t[6] - t[5], t[0] - h[0],
+                u[1] - u[0], u[2] - u[1], u[3] - u[2], i ? u[0] - (u - 4)[3] : 0LL);
+      }
+      for (int b = 0; b < 2; ++b)
+        for (int q = 0; q < 64; ++q) {
+          const long long* u = h + 6144 + (b * 64 + q) * 4;
+          if (u[0]) fprintf(f, "recheck cta %d q %2d: xload %6lld chain %6lld cand %lld\n", b, q, u[2] - u[0], u[1] - u[2], u[3]);
+        }
+      if (resident) {  // per-pass phase ends of the resident loop (ns, max over CTAs, from CTA 0's start)
+        const unsigned long long* q = reinterpret_cast<const unsigned long long*>(h + 4096);
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int cnt = 0;
+        for (int it = 20; it < 256; ++it) {
+          const unsigned long long* u = q + it * 8;
+          if (!u[7] || !u[6]) break;
+          for (int j = 1; j < 8; ++j) acc[j] += (double)(long long)(u[j] - u[0]);
+          ++cnt;
+        }
+        if (cnt)
+          fprintf(f, "resident passes 20..%d (ns after CTA0 start): main %.0f recheck %.0f flush %.0f arrive %.0f "
+                  "divide %.0f conv %.0f prep %.0f\n", 20 + cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+                  acc[4] / cnt, acc[5] / cnt, acc[6] / cnt, acc[7] / cnt);
       }
       fprintf(f, "----\n");
       fclose(f);

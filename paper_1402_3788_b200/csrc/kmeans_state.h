@@ -28,8 +28,8 @@ __device__ __forceinline__ void smem_add64(unsigned long long* addr, unsigned lo
   unsigned int* p = reinterpret_cast<unsigned int*>(addr);
   const unsigned int lo = (unsigned int)v, hi = (unsigned int)(v >> 32);
   const unsigned int old = atomicAdd(p, lo);
-  const unsigned int h = hi + ((old + lo) < old ? 1u : 0u);
-  if (h) atomicAdd(p + 1, h);
+  // unconditional (no branch on the returned value): independent adds pipeline
+  atomicAdd(p + 1, hi + ((old + lo) < old ? 1u : 0u));
 }
 
 #endif

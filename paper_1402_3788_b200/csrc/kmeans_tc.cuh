@@ -19,9 +19,10 @@
 // per CTA); the finish kernel folds Δ into the running totals.  The first
 // pass (no previous labels) adds every point.
 //
-// Points whose label the filter cannot certify are queued and re-decided by
-// recheck_kernel (the reference's exact fp64 recurrence over all centres), so
-// the rare slow path never stalls the pipelined hot loop.
+// Points whose label the filter cannot certify are re-decided in the epilogue
+// with the reference's exact fp64 recurrence over the candidate centres (those
+// whose filter score lies within 2E of the best; every other centre is strictly
+// farther), which the HBM-bound pipeline absorbs.
 //
 // Warp roles (persistent CTA, one per SM), pipelined over 128-point tiles:
 //   warps 0-7  : transform   two groups, alternate tiles: raw tile → fp16 [hi|lo] A operand
@@ -42,20 +43,35 @@
 namespace km {
 namespace tc {
 
+constexpr int kQueueCap = 768;                     // per-CTA staging of uncertified points (smem)
+constexpr int kTileRows = 128;
 constexpr int kTransformGroups = 2;                // transform warpgroups (alternate tiles)
 constexpr int kTransformWarps = 4 * kTransformGroups;
 constexpr int kEpiGroups = 2;                      // epilogue warpgroups (alternate tiles)
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kProducerWarp = kTransformWarps + kEpiWarps;  // TMA producer
-constexpr int kMmaWarp = kProducerWarp + 1;                 // TMEM allocator + MMA issuer
-constexpr int kThreadsTC = (kMmaWarp + 1) * 32;
-constexpr int kQueueCap = 1024;                    // per-CTA staging of uncertified points (smem)
-// ring depths: raw tiles in flight (TMA → transform) and A operand buffers (transform → MMA);
-// shallower for the widest shapes so the CTA fits in 227 KB of shared memory
+constexpr int kMmaWarp = kProducerWarp + 1;                 // TMEM allocator + MMA issuer (even tiles)
+constexpr int kMmaWarps = 2;                                // issuers: tile g → warp kMmaWarp + g % 2
+constexpr int kThreadsTC = (kMmaWarp + kMmaWarps) * 32;
+// Ring depths.  The pass is HBM bound, so the raw ring (TMA → transform) gets every byte of
+// shared memory the other sections leave (≥ ~64 KB in flight per SM covers the loaded DRAM
+// latency); the A ring (transform → MMA) only has to cover the short MMA.
 template <int MP, int KP>
 struct TcStages {
-  static constexpr int raw = (MP <= 23 && KP <= 32) ? 6 : 4;
-  static constexpr int a = (MP <= 23 && KP <= 32) ? 6 : 4;
+  static constexpr int a = 4;
+  static constexpr int mw = (KP + 31) / 32;
+  static constexpr int raw_stride_max = ((kTileRows * MP * 4 + 256 + 1023) / 1024) * 1024;
+  static constexpr int fixed = a * kTileRows * 128 + 2 * KP * 128 +                      // A ring, B tile
+                               ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024 +       // Δ accumulators
+                               kQueueCap * (8 + 4 * mw) + 1024 +                       // recheck queue
+                               2048 + 1024 + 8192;                                     // barriers, align, static
+  static constexpr int cres = ((2 * KP * MP * 8) + 1023) / 1024 * 1024;                // resident centres
+  // keep room for the resident loop's centres unless that would starve the raw ring
+  // (the widest shapes then run launch-per-iteration)
+  static constexpr int fit_res = (227 * 1024 - fixed - cres) / raw_stride_max;
+  static constexpr int fit = fit_res >= 4 ? fit_res : (227 * 1024 - fixed) / raw_stride_max;
+  static constexpr int raw = fit > 12 ? 12 : fit;
+  static_assert(raw >= 3, "shared-memory budget");
 };
 
 // ---- PTX helpers -----------------------------------------------------------
@@ -123,6 +139,39 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// streaming copy: the points are read once per pass, so they should not push the labels,
+// the totals and the rows queued for re-decision out of L2
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                              uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_l2_keep(const void* p) {
+  asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(p));
+}
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n"
+      ".reg .b32 rx;\n"
+      ".reg .pred px;\n"
+      "elect.sync rx|px, 0xffffffff;\n"
+      "selp.b32 %0, 1, 0, px;\n"
+      "}\n"
+      : "+r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_barrier_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -247,29 +296,12 @@ struct TcSmem {
     off_a = RS * raw_stride;                 // [AS][128 rows × 128 B]
     off_w = off_a + AS * kTile * 128;        // [2KP rows × 128 B]
     off_acc = off_w + 2 * KP * 128;          // [KP·(MP+1) + KP] int64 Δ accumulators
-    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // [kQueueCap] int64 rows + counters
-    off_c = off_q + kQueueCap * 8 + 1024;    // [2][kres·m] fp64 centres (resident)
+    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // recheck queue: rows, masks, scalars
+    off_c = off_q + kQueueCap * (8 + 4 * ((KP + 31) / 32)) + 1024;  // [2][kres·m] fp64 centres (resident)
     off_bar = off_c + ((uint32_t)(2 * kres * m * 8) + 1023) / 1024 * 1024;
     total = off_bar + 1024 + 1024;           // barriers + 1 KiB alignment slack
   }
 };
-
-// Exact label of one point by one thread (overflow of the CTA's recheck queue; rare):
-// the reference recurrence (features ascending, no FMA, strict '<' → lowest index).
-static __device__ __noinline__ int exact_label_thread(const float* __restrict__ xr, int m, int k,
-                                               const double* __restrict__ C) {
-  double bd = 0.0;
-  int bl = -1;
-  for (int c = 0; c < k; ++c) {
-    double acc = 0.0;
-    for (int f = 0; f < m; ++f) {
-      const double d = __dsub_rn((double)__ldg(xr + f), C[(size_t)c * m + f]);
-      acc = __dadd_rn(acc, __dmul_rn(d, d));
-    }
-    if (bl < 0 || acc < bd) { bd = acc; bl = c; }
-  }
-  return bl;
-}
 
 __device__ __forceinline__ unsigned int ld_acquire_u32(const unsigned int* p) {
   unsigned int v;
@@ -334,6 +366,50 @@ __device__ __forceinline__ void cta_prep_operand(const double* __restrict__ C, i
   __syncthreads();
 }
 
+// Exact label of one point by one thread over its candidate centres (bit set in mk):
+// the reference recurrence (features ascending, no FMA) per centre, centres ascending,
+// strict '<' (lowest index on ties).  Non-candidates are strictly farther than the best
+// candidate (filter bound), so the result equals the reference's argmin over all k.
+template <int MP, int MW>
+__device__ __forceinline__ int exact_candidates(const float* __restrict__ gx, int m, const double* __restrict__ C,
+                                                const uint32_t (&mk)[MW], float (&xr)[MP],
+                                                long long* ts = nullptr) {
+#pragma unroll
+  for (int f = 0; f < MP; ++f) xr[f] = (f < m) ? __ldg(gx + f) : 0.f;
+  if (ts) {
+    float sx = 0.f;
+#pragma unroll
+    for (int f = 0; f < MP; ++f) sx += xr[f];
+    ts[0] = clock64() + (sx == 12345.f);
+  }
+  double bd = 0.0;
+  int bl = -1;
+#pragma unroll 1
+  for (int w = 0; w < MW; ++w) {
+    uint32_t bits = mk[w];
+#pragma unroll 1
+    while (bits) {
+      const int c = w * 32 + __ffs(bits) - 1;
+      bits &= bits - 1;
+      // the candidate's row first (all loads in flight together), then the dependent chain
+      const double* cr = C + (size_t)c * m;
+      double cv[MP];
+#pragma unroll
+      for (int f = 0; f < MP; ++f) cv[f] = (f < m) ? cr[f] : 0.0;
+      double acc = 0.0;
+#pragma unroll
+      for (int f = 0; f < MP; ++f) {
+        if (f < m) {
+          const double d = __dsub_rn((double)xr[f], cv[f]);
+          acc = __dadd_rn(acc, __dmul_rn(d, d));
+        }
+      }
+      if (bl < 0 || acc < bd) { bd = acc; bl = c; }
+    }
+  }
+  return bl;
+}
+
 // MT > 0: exact feature count m = MT (compile-time); MT < 0: runtime m ≤ −MT.
 // PRE: multiply x by the power-of-two prescale (off when the data range is fp16-safe as is).
 //
@@ -347,7 +423,7 @@ __device__ __forceinline__ void cta_prep_operand(const double* __restrict__ C, i
 //   clusters (the host repairs them and relaunches).
 template <int MT, int KP, bool PRE>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
-  static_assert(kThreadsTC == 576, "warp-role layout");
+  static_assert(kThreadsTC == 608, "warp-role layout");
   constexpr int MP = MT > 0 ? MT : -MT;
   if (a.gate && (a.st->done || a.st->need_host)) return;
   using L = TcLayout<MP>;
@@ -362,9 +438,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   float* raw = reinterpret_cast<float*>(sm + S.off_raw);
   unsigned char* s_w = sm + S.off_w;
   unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(sm + S.off_acc);
-  long long* s_q = reinterpret_cast<long long*>(sm + S.off_q);
-  unsigned int* s_qn = reinterpret_cast<unsigned int*>(sm + S.off_q + kQueueCap * 8);  // [0] queue length
-  float* s_cmax = reinterpret_cast<float*>(s_qn + 4);                                  // resident: max ‖c‖
+  constexpr int MW = (KP + 31) / 32;                                          // candidate mask words
+  long long* s_q = reinterpret_cast<long long*>(sm + S.off_q);                 // [cap] row << 8 | old + 1
+  uint32_t* s_qm = reinterpret_cast<uint32_t*>(sm + S.off_q + kQueueCap * 8);  // [cap][MW] candidate masks
+  unsigned int* s_qn = s_qm + kQueueCap * MW;                                  // [0] queue length
+  float* s_cmax = reinterpret_cast<float*>(s_qn + 4);                          // resident: max ‖c‖
   double* s_cbuf = reinterpret_cast<double*>(sm + S.off_c);                            // resident: [2][k·m]
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S.off_bar);
   uint64_t* full_raw = bars;                 // [RS] TMA → transform
@@ -380,7 +458,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   const int km = k * m;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (a.n + kTile - 1) / kTile;
-  const int my_tiles = (int)((ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x);
+  // contiguous tile range per CTA: [t_lo, t_lo + my_tiles) (TLB- and DRAM-page-friendly streams)
+  const int64_t t_lo = ntiles * blockIdx.x / gridDim.x;
+  const int my_tiles = (int)(ntiles * (blockIdx.x + 1) / gridDim.x - t_lo);
   const int nacc = km + k;
   const int npre = resident ? min(RS, my_tiles) : 0;  // next-pass tiles streamed during the tail
 
@@ -437,48 +517,62 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   int g0 = 0;      // tiles of earlier passes (ring positions continue across passes)
   int issued = 0;  // producer: tiles of the current pass already in flight
 
+  // tuning only: per-pass phase ends (globaltimer, max over CTAs) of the resident loop
+  unsigned long long* pst = (a.dbg_times != nullptr && resident && tid == 0)
+                                ? reinterpret_cast<unsigned long long*>(a.dbg_times + 4096) : nullptr;
   for (int it = 0;; ++it) {
     const double* C = resident ? s_cbuf + cb * km : a.c64;
+    if (pst && it < 256 && blockIdx.x == 0) pst[it * 8 + 0] = globaltimer();
     if (warp == kProducerWarp) {
       // ===================== TMA producer: tile g → raw slot g % RS =====================
       if (lane == 0) {
+        const uint64_t pol = l2_policy_evict_first();
         auto issue = [&](int g, int i) {
           const int s = g % RS;
           if (g >= RS) mbar_wait(empty_raw + s, ((g / RS) - 1) & 1);
-          const int64_t row0 = (blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+          const int64_t row0 = (t_lo + i) * kTile;
           const int64_t rem = a.n - row0;
           const int rows = rem < kTile ? (int)rem : kTile;
           const uint32_t bytes = ((uint32_t)rows * m * 4u) & ~15u;
           mbar_arrive_expect_tx(full_raw + s, bytes);
           if (bytes)
-            bulk_g2s(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes, full_raw + s);
+            bulk_g2s_hint(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes, full_raw + s,
+                          pol);
         };
         for (int i = issued; i < my_tiles; ++i) issue(g0 + i, i);
         for (int j = 0; j < npre; ++j) issue(g0 + my_tiles + j, j);  // next pass (resident)
       }
       issued = npre;
-    } else if (warp == kMmaWarp) {
-      // ===================== MMA issuer (one thread) =====================
-      if (lane == 0) {
-        const uint32_t a0 = smem_u32(sm + S.off_a), w0 = smem_u32(s_w);
-        constexpr uint32_t idesc = idesc_f16(2 * KP);
-        for (int i = 0; i < my_tiles; ++i) {
-          const int g = g0 + i;
-          const int sa = g % AS, ss = g % TM::NS;
-          mbar_wait(a_full + sa, (g / AS) & 1);
-          if (g >= TM::NS) mbar_wait(s_empty + ss, ((g / TM::NS) - 1) & 1);
-          tc_fence_after();
-          const uint32_t ag = a0 + sa * (kTile * 128);
-          const uint32_t dcol = tmem + ss * 2 * KP;
+    } else if (warp >= kMmaWarp) {
+      // ===================== MMA issuers: warp kMmaWarp + j takes tiles g ≡ j (mod 2); the whole warp
+      // runs the (uniform) loop, one elected lane issues (per-tile issue cost halves per warp) =====================
+      const int mj = warp - kMmaWarp;
+      const uint32_t a0 = smem_u32(sm + S.off_a), w0 = smem_u32(s_w);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform → uniform registers
+      constexpr uint32_t idesc = idesc_f16(2 * KP);
+      const uint64_t bdesc0 = make_desc(w0, 16, 1024);
+      for (int i = (mj - (g0 & 1)) & 1; i < my_tiles; i += kMmaWarps) {
+        const int g = g0 + i;
+        const int sa = g % AS, ss = g % TM::NS;
+        long long* ms = (a.dbg_times != nullptr && blockIdx.x == 0 && i < 64 && lane == 0 && it == (resident ? 100 : 0))
+                            ? a.dbg_times + 3072 + i * 4 : nullptr;
+        if (ms) ms[0] = clock64();
+        mbar_wait(a_full + sa, (g / AS) & 1);
+        if (ms) ms[1] = clock64();
+        if (g >= TM::NS) mbar_wait(s_empty + ss, ((g / TM::NS) - 1) & 1);
+        if (ms) ms[2] = clock64();
+        tc_fence_after();
+        const uint64_t adesc0 = make_desc(a0 + sa * (kTile * 128), 16, 1024);
+        const uint32_t dcol = tm + ss * 2 * KP;
+        if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < L::KSTEPS; ++ks) {
-            if (a.dbg_flags & 2) break;
-            mma_f16(dcol, make_desc(ag + ks * 32, 16, 1024), make_desc(w0 + ks * 32, 16, 1024), idesc,
-                    ks > 0 ? 1u : 0u);
-          }
+          for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
+            mma_f16(dcol, adesc0 + 2 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
           mma_commit(s_full + ss);   // scores ready
           mma_commit(a_empty + sa);  // A buffer consumed
         }
+        __syncwarp();
+        if (ms) ms[3] = clock64();
       }
     } else if (warp < kTransformWarps) {
       // ===================== transform: thread = point; group tg takes tiles g ≡ tg (mod 2) =====================
@@ -490,12 +584,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       for (int i = (tg - (g0 & 1)) & 1; i < my_tiles; i += kTransformGroups) {
         const int g = g0 + i;
         const int s = g % RS, sa = g % AS;
-        const int64_t row0 = (blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+        const int64_t row0 = (t_lo + i) * kTile;
         const int64_t rem = a.n - row0;
         const int rows = rem < kTile ? (int)rem : kTile;
         const bool active = p < rows;
-        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && g < 64;
-        long long* ts = stamp ? a.dbg_times + (size_t)g * 8 : nullptr;
+        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
+        long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[0] = clock64();
         mbar_wait(full_raw + s, (g / RS) & 1);
         if (stamp) ts[1] = clock64();
@@ -565,10 +659,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const float inv_pre2 = 1.0f / (pre * pre);
       const double scale_d = a.scale_d;
       const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0;
-      unsigned int my_changed = 0;
+      unsigned int my_changed = 0, my_rechecked = 0;
       auto prev_label = [&](int i) -> int {  // previous label of this thread's point in tile i (or -1)
         if (full || i >= my_tiles) return -1;
-        const int64_t r = (blockIdx.x + (int64_t)i * gridDim.x) * kTile + p;
+        const int64_t r = (t_lo + i) * kTile + p;
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
       const int i0 = (e - (g0 & 1)) & 1;
@@ -576,14 +670,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       for (int i = i0; i < my_tiles; i += kEpiGroups) {
         const int g = g0 + i;
         const int ss = g % TM::NS;
-        const int64_t row0 = (blockIdx.x + (int64_t)i * gridDim.x) * kTile;
+        const int64_t row0 = (t_lo + i) * kTile;
         const int64_t rem = a.n - row0;
         const int rows = rem < kTile ? (int)rem : kTile;
         const bool active = p < rows;
         const int old = old_next;
         old_next = prev_label(i + kEpiGroups);  // prefetch one tile ahead (global latency off the critical path)
-        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && g < 64;
-        long long* ts = stamp ? a.dbg_times + (size_t)g * 8 : nullptr;
+        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
+        long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[4] = clock64();
         mbar_wait(s_full + ss, (g / TM::NS) & 1);
         if (stamp) ts[5] = clock64();
@@ -627,22 +721,48 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           bi = rb ? ix[0] : bi;
           best = rb ? v[0] : best;
         }
+        const bool unc = active && (exact_only || !(min2 > best + E2));
+        if (__any_sync(0xffffffffu, unc)) {
+          // uncertified: only centres whose filter score lies within 2E of the best can be the
+          // reference's argmin (every other one is strictly farther) — collect them as a mask
+          // (second look at the scores) and queue the point for the exact re-decision
+          const float thr = exact_only ? __int_as_float(0x7f800000) : best + E2;
+          uint32_t mk[MW];
+#pragma unroll
+          for (int w = 0; w < MW; ++w) mk[w] = 0u;
+#pragma unroll
+          for (int c0 = 0; c0 < KP; c0 += 16) {
+            uint32_t r0[16], r1[16];
+            tmem_ld16(tmem + lane_base + ss * 2 * KP + c0, r0);
+            tmem_ld16(tmem + lane_base + ss * 2 * KP + KP + c0, r1);
+            tmem_ld_wait();
+            uint32_t bits = 0;
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj)
+              bits |= (__uint_as_float(r0[jj]) + __uint_as_float(r1[jj]) <= thr && c0 + jj < k) ? (1u << jj) : 0u;
+            mk[c0 >> 5] |= bits << (c0 & 31);
+          }
+          if (unc) {
+            ++my_rechecked;
+            const unsigned int slot = atomicAdd(s_qn, 1u);
+            if (slot < kQueueCap) {
+              s_q[slot] = ((row0 + p) << 8) | (long long)(old + 1);  // row | previous label + 1 (0 = none)
+              const float* gr = a.x + (row0 + p) * m;  // keep the row in L2 until the tail reads it
+              prefetch_l2_keep(gr);
+              prefetch_l2_keep(gr + m - 1);
+#pragma unroll
+              for (int w = 0; w < MW; ++w) s_qm[slot * MW + w] = mk[w];
+              bi = old;  // decided in the tail
+            } else {     // staging full (rare): decide here
+              float xq[MP];
+              bi = exact_candidates<MP, MW>(a.x + (row0 + p) * m, m, C, mk, xq);
+            }
+          }
+        }
         tc_fence_before();  // TMEM reads ordered before the MMA reuses this buffer
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty + ss);
-        const bool certified = !exact_only && (min2 > best + E2);
-        bool apply = active && certified && bi != old;
-        if (active && !certified) {
-          // defer to the CTA's tail (warp-cooperative exact re-decision)
-          const unsigned int slot = atomicAdd(s_qn, 1u);
-          if (slot < kQueueCap) {
-            s_q[slot] = ((row0 + p) << 24) | (long long)(old + 1);  // row | previous label (+1; 0 = none)
-          } else {  // staging full (rare): decide it here, thread-serial
-            bi = exact_label_thread(a.x + (row0 + p) * m, m, k, C);
-            apply = bi != old;
-          }
-        }
-        if (apply) {
+        if (active && bi != old) {
           // --- exact incremental update of the per-cluster fixed-point sums
           ++my_changed;
           a.labels[row0 + p] = bi;
@@ -659,64 +779,58 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         }
         if (stamp) ts[6] = clock64();
       }
-      if (!full) {
-        unsigned int w2 = my_changed;
+      unsigned int w2 = full ? 0u : my_changed, w3 = my_rechecked;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) w2 += __shfl_xor_sync(0xffffffffu, w2, o);
-        if (lane == 0 && w2) atomicAdd(&st->changed, (unsigned long long)w2);
+      for (int o = 16; o > 0; o >>= 1) {
+        w2 += __shfl_xor_sync(0xffffffffu, w2, o);
+        w3 += __shfl_xor_sync(0xffffffffu, w3, o);
       }
+      if (lane == 0 && w2) atomicAdd(&st->changed, (unsigned long long)w2);
+      if (lane == 0 && w3) atomicAdd(&st->rechecked, (unsigned long long)w3);
     }
     // ===================== tail (all warps) =====================
     tc_fence_before();
-    __syncthreads();  // every role done with this pass: Δ atomics and the CTA's recheck queue are complete
-    const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
-    const double* Cx = C;  // fp64 centres of the pass for the exact re-decision
+    __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
+    if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
     double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
     const int stage_cap = (int)(RS * S.raw_stride / 8);
-    if (!resident && qn && km <= stage_cap) {
-      // the raw ring is idle now (no next-pass prefetch): stage the fp64 centres there
-      for (int i = tid; i < km; i += kThreadsTC) s_stage[i] = a.c64[i];
-      __syncthreads();
-      Cx = s_stage;
-    }
     {
-      // exact re-decision of this CTA's uncertified points, 4 per warp (x rows fetched together), Δ into s_acc
-      for (unsigned int q0 = warp * 4; q0 < qn; q0 += (kThreadsTC / 32) * 4) {
-        long long ent[4];
-        float xb[4];
+      // exact re-decision of the queued points: thread per point over its candidate centres
+      const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
+      for (unsigned int q = tid; q < qn; q += kThreadsTC) {
+        const long long ent = s_q[q];
+        const long long row = ent >> 8;
+        const int old = (int)(ent & 0xff) - 1;
+        uint32_t mk[MW];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          ent[j] = (q0 + j < qn) ? s_q[q0 + j] : -1;
-          xb[j] = (ent[j] >= 0 && lane < m) ? __ldg(a.x + (ent[j] >> 24) * m + lane) : 0.f;
-        }
-        int lb[4];
-        exact_label_warp_batch<MP, 4>(xb, m, k, Cx, lb);
+        for (int w = 0; w < MW; ++w) mk[w] = s_qm[q * MW + w];
+        long long* qs = (a.dbg_times != nullptr && blockIdx.x < 4 && it == 100 && q < 64)
+                            ? a.dbg_times + 6144 + (blockIdx.x * 64 + q) * 4 : nullptr;
+        if (qs) qs[0] = clock64();
+        float xq[MP];
+        const int bl = resident ? exact_candidates<MP, MW>(a.x + row * m, m, s_cbuf + cb * km, mk, xq, qs ? qs + 2 : nullptr)
+                                : exact_candidates<MP, MW>(a.x + row * m, m, a.c64, mk, xq);
+        if (qs) { qs[1] = clock64() + (bl == 12345); qs[3] = __popc(mk[0]) + 100 * (bl != old); }
+        if (bl != old) {
+          a.labels[row] = bl;
+          if (!full) atomicAdd(&st->changed, 1ull);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (ent[j] < 0) continue;
-          const long long row = ent[j] >> 24;
-          const float xl = xb[j];
-          const int bl = lb[j];
-          const int old = full ? -1 : (int)(ent[j] & 0xffffff) - 1;
-          if (bl != old) {
-            if (lane == 0) {
-              a.labels[row] = bl;
-              smem_add64(s_acc + (size_t)km + bl, 1ull);
-              if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
-              if (!full) atomicAdd(&st->changed, 1ull);
-            }
-            if (lane < m) {
-              const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xl, a.scale_d))
-                                               : __float2ll_rn(__fmul_rn(xl, a.scale_f));
-              smem_add64(s_acc + (size_t)bl * m + lane, (unsigned long long)v);
-              if (old >= 0) smem_add64(s_acc + (size_t)old * m + lane, (unsigned long long)(-v));
+          for (int f = 0; f < MP; ++f) {
+            if (f < m) {
+              const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
+                                               : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
+              smem_add64(s_acc + (size_t)bl * m + f, (unsigned long long)v);
+              if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
             }
           }
+          smem_add64(s_acc + (size_t)km + bl, 1ull);
+          if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
         }
       }
-      if (tid == 0 && s_qn[0]) atomicAdd(&st->rechecked, (unsigned long long)s_qn[0]);
+      __syncthreads();
+      if (tid == 0) s_qn[0] = 0u;
+      if (pst && it < 256) atomicMax(pst + it * 8 + 2, globaltimer());
     }
-    __syncthreads();
     if (!resident) {
       for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
         const unsigned long long v = s_acc[i];
@@ -749,8 +863,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     }
     __threadfence();
     __syncthreads();
+    if (pst && it < 256) atomicMax(pst + it * 8 + 3, globaltimer());
+    if (pst && it < 256) atomicMax(pst + it * 8 + 4, globaltimer());
     if (tid == 0) {
-      s_qn[0] = 0u;
       atomicAdd(a.grid_sync, 1u);
       grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
     }
@@ -768,55 +883,110 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       stop = true;
     } else {
       double* Cn = s_cbuf + (cb ^ 1) * km;
-      for (int i = tid; i < km; i += kThreadsTC) {
-        const long long nc = (long long)__ldcg(tot + km + i / m);
-        const long long sv = (long long)__ldcg(tot + i);
+      // warp per centre, lane per feature: C_{t+1} = S/N, the congruence terms, ‖fl32(c)‖² and the
+      // centre's two B-operand rows in one pass (no per-centre serial loops on the critical path)
+      __shared__ float s_wmax[32];
+      __shared__ int s_wflags[32];  // bit 0: some cluster empty, bit 1: some centre moved
+      const int hw = 8 * ((m + 1 + 7) / 8);
+      float wmax = 0.f;
+      int wflags = 0;
+      for (int c = warp; c < k; c += kThreadsTC / 32) {
+        const long long nc = (long long)__ldcg(tot + km + c);
+        const bool fv = lane < m;
+        const long long sv = fv ? (long long)__ldcg(tot + (size_t)c * m + lane) : 0ll;
         // empty clusters get a placeholder; every one is re-seeded by the host repair
-        Cn[i] = nc > 0 ? __ddiv_rn(__dmul_rn((double)sv, a.fin.inv_scale), (double)nc) : 0.0;
+        const double v = (fv && nc > 0) ? __ddiv_rn(__dmul_rn((double)sv, a.fin.inv_scale), (double)nc) : 0.0;
+        const double vo = fv ? C[(size_t)c * m + lane] : 0.0;
+        if (fv) Cn[(size_t)c * m + lane] = v;
+        if (pub) {
+          if (fv) {
+            a.fin.prev[(size_t)c * m + lane] = vo;
+            a.fin.cur[(size_t)c * m + lane] = v;
+          }
+          if (lane == 0) a.fin.model_counts[c] = nc;
+        }
+        // congruence (engine.converged): sqrt(Σ_f (prev − next)², features ascending) ≤ tol
+        const double dd = fv ? __dmul_rn(__dsub_rn(vo, v), __dsub_rn(vo, v)) : 0.0;
+        bool moved;
+        if (tol == 0.0) {
+          moved = __any_sync(0xffffffffu, dd != 0.0);  // a sum of non-negative terms is 0 iff every term is
+        } else {
+          double acc = 0.0;
+          for (int f = 0; f < m; ++f) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, dd, f));
+          moved = !(sqrt(acc) <= tol);
+        }
+        wflags |= (nc == 0 ? 1 : 0) | (moved ? 2 : 0);
+        // filter operand: ‖fl32(c)‖² (fp64, exact squares, fixed tree order), max ‖c‖ rounded up
+        const double q = fv ? (double)__double2float_rn(v) : 0.0;
+        double cn2 = q * q;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) cn2 += __shfl_xor_sync(0xffffffffu, cn2, o);
+        wmax = fmaxf(wmax, __double2float_ru(sqrt(cn2) * (1.0 + 1e-12)));
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int col = lane + 32 * h;
+          const int f = col < hw ? col : col - hw;
+          const double vf = __shfl_sync(0xffffffffu, v, f < 32 ? f : 0);
+          float w = 0.f;
+          if (col < 2 * hw) {
+            if (f < m) w = -2.0f * __double2float_rn(vf) * pre;
+            else if (f == m) w = __double2float_rn(cn2 * (double)pre * (double)pre);
+          }
+          const __half wh = __float2half_rn(w);
+          const __half wl = __float2half_rn(w - __half2float(wh));
+          *reinterpret_cast<unsigned short*>(s_w + sw128(c, col >> 3) + (col & 7) * 2) =
+              (col < 2 * hw) ? __half_as_ushort(wh) : (unsigned short)0;
+          *reinterpret_cast<unsigned short*>(s_w + sw128(KP + c, col >> 3) + (col & 7) * 2) =
+              (col < hw) ? __half_as_ushort(wl) : (unsigned short)0;
+        }
       }
-      long long nc_mine = 0;
-      if (tid < k) nc_mine = (long long)__ldcg(tot + km + tid);
-      const int n_empty = __syncthreads_count(tid < k && nc_mine == 0);  // also: Cn complete
+      fence_proxy_async();  // B-operand rows → visible to the tensor core after the barrier
+      if (lane == 0) {
+        s_wmax[warp] = wmax;
+        s_wflags[warp] = wflags;
+      }
+      __syncthreads();
+      if (pst && it < 256) atomicMax(pst + it * 8 + 5, globaltimer());
       if (tid == 0) {  // this CTA is done reading the totals
         __threadfence();
         atomicAdd(a.grid_sync + 1, 1u);
       }
-      ++t_upd;
-      if (pub) {
-        for (int i = tid; i < km; i += kThreadsTC) {
-          a.fin.prev[i] = C[i];
-          a.fin.cur[i] = Cn[i];
-        }
-        if (tid < k) a.fin.model_counts[tid] = nc_mine;
-        if (tid == 0) {
-          st->t = t_upd;
-          st->n_empty = n_empty;
-        }
+      int flags = 0;
+      float cmx = 0.f;
+      for (int w = 0; w < kThreadsTC / 32; ++w) {
+        flags |= s_wflags[w];
+        cmx = fmaxf(cmx, s_wmax[w]);
       }
-      if (n_empty > 0) {
-        if (pub && tid == 0) st->need_host = 1;
+      ++t_upd;
+      if (pub && tid == 0) st->t = t_upd;
+      if (flags & 1) {
+        if (pub && tid == 0) {
+          int ne = 0;
+          for (int c = 0; c < k; ++c) ne += (__ldcg(tot + km + c) == 0ull);
+          st->n_empty = ne;
+          st->need_host = 1;
+        }
+        stop = true;
+      } else if (!(flags & 2)) {
+        if (pub && tid == 0) {
+          st->n_empty = 0;
+          st->converged = 1;
+          st->done = 1;
+        }
         stop = true;
       } else {
-        __shared__ double s_redd[32];
-        const int conv = block_converged(C, Cn, k, m, tol, s_redd);
-        if (conv) {
-          if (pub && tid == 0) {
-            st->converged = 1;
-            st->done = 1;
-          }
-          stop = true;
-        } else {
-          if (t_upd >= max_iters) {  // reference: one more assign pass, then return
-            exhausted = true;
-            if (pub && tid == 0) st->exhausted = 1;
-          }
-          cta_prep_operand(Cn, k, m, KP, pre, s_w, s_cmax);
-          cb ^= 1;
-          full = false;
+        if (t_upd >= max_iters) {  // reference: one more assign pass, then return
+          exhausted = true;
+          if (pub && tid == 0) st->exhausted = 1;
         }
+        if (tid == 0) s_cmax[0] = cmx;
+        cb ^= 1;
+        full = false;
       }
+      if (pst && it < 256) atomicMax(pst + it * 8 + 6, globaltimer());
     }
     __syncthreads();
+    if (pst && it < 256) atomicMax(pst + it * 8 + 7, globaltimer());
     if (stop) break;
     g0 += my_tiles;
   }
