@@ -280,18 +280,30 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
     if (f) {
       for (int i = 0; i < 64; ++i) {
         if (!h[i * 8]) continue;
-        const long long* t = h + i * 8;  // transform: raw wait, compute, A-buffer wait, store; epilogue: s wait, body
-        const long long* u = h + 3072 + i * 4;
-        fprintf(f, "tile %2d  T: raw %5lld comp %5lld awaitA %5lld sts %5lld | E: swait %5lld body %5lld | t0 %lld"
-                "  | M: afull-wait %lld sempty-wait %lld issue %lld  loop %lld\n", i,
-                t[1] - t[0], t[7] - t[1], t[2] - t[7], t[3] - t[2], t[5] - t[4], t[6] - t[5], t[0] - h[0],
-                u[1] - u[0], u[2] - u[1], u[3] - u[2], i ? u[0] - (u - 4)[3] : 0LL);
+        const long long* t = h + i * 8;  // transform: 0 start, 1 raw ok, 7 raw released, 2 A ok, 3 a_full; epilogue: 4 start, 5 got, 6 done
+        const long long* u = h + 3072 + i * 4;  // MMA: 0 start, 1 a_full ok, 2 s_empty ok, 3 issued
+        const long long z = h[0];
+        fprintf(f, "tile %2d T[%6lld raw+%4lld comp+%4lld A+%4lld sts+%4lld] M[%6lld af+%4lld se+%4lld is+%4lld] E[%6lld got+%4lld body+%4lld]\n", i,
+                t[0] - z, t[1] - t[0], t[7] - t[1], t[2] - t[7], t[3] - t[2], u[0] - z, u[1] - u[0], u[2] - u[1], u[3] - u[2],
+                t[4] - z, t[5] - t[4], t[6] - t[5]);
       }
-      for (int b = 0; b < 2; ++b)
-        for (int q = 0; q < 64; ++q) {
-          const long long* u = h + 6144 + (b * 64 + q) * 4;
-          if (u[0]) fprintf(f, "recheck cta %d q %2d: xload %6lld chain %6lld cand %lld\n", b, q, u[2] - u[0], u[1] - u[2], u[3]);
+      if (resident && h[6144]) {  // per-CTA main loop of pass 100 (ns)
+        long long s0 = h[6144], s1 = h[6144], dmin = 1ll << 60, dmax = 0, dsum = 0, e1 = 0;
+        int nb = 0, bmax = 0;
+        for (int b = 0; b < 148 && h[6144 + 2 * b]; ++b, ++nb) {
+          const long long st0 = h[6144 + 2 * b], en = h[6144 + 2 * b + 1], d = en - st0;
+          s0 = std::min(s0, st0); s1 = std::max(s1, st0); e1 = std::max(e1, en);
+          dmin = std::min(dmin, d); dsum += d;
+          if (d > dmax) { dmax = d; bmax = b; }
         }
+        fprintf(f, "pass 100 main loop per CTA (ns): min %lld avg %lld max %lld (cta %d)  start skew %lld  span %lld\n",
+                dmin, dsum / std::max(1, nb), dmax, bmax, s1 - s0, e1 - s0);
+        for (int b = 0; b < nb; b += 8) {
+          fprintf(f, "  cta %3d..:", b);
+          for (int j = b; j < std::min(nb, b + 8); ++j) fprintf(f, " %6lld", h[6144 + 2 * j + 1] - h[6144 + 2 * j]);
+          fprintf(f, "\n");
+        }
+      }
       if (resident) {  // per-pass phase ends of the resident loop (ns, max over CTAs, from CTA 0's start)
         const unsigned long long* q = reinterpret_cast<const unsigned long long*>(h + 4096);
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -44,6 +44,7 @@ namespace km {
 namespace tc {
 
 constexpr int kQueueCap = 768;                     // per-CTA staging of uncertified points (smem)
+constexpr long long kQueueFlag = 1ll << 62;
 constexpr int kTileRows = 128;
 constexpr int kTransformGroups = 2;                // transform warpgroups (alternate tiles)
 constexpr int kTransformWarps = 4 * kTransformGroups;
@@ -52,16 +53,18 @@ constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kProducerWarp = kTransformWarps + kEpiWarps;  // TMA producer
 constexpr int kMmaWarp = kProducerWarp + 1;                 // TMEM allocator + MMA issuer (even tiles)
 constexpr int kMmaWarps = 2;                                // issuers: tile g → warp kMmaWarp + g % 2
-constexpr int kThreadsTC = (kMmaWarp + kMmaWarps) * 32;
-// Ring depths.  The pass is HBM bound, so the raw ring (TMA → transform) gets every byte of
-// shared memory the other sections leave (≥ ~64 KB in flight per SM covers the loaded DRAM
-// latency); the A ring (transform → MMA) only has to cover the short MMA.
-template <int MP, int KP>
-struct TcStages {
-  static constexpr int a = 4;
+constexpr int kRecheckWarp = kMmaWarp + kMmaWarps;          // exact re-decision of queued points, during the pass
+constexpr int kThreadsTC = (kRecheckWarp + 1) * 32;
+// Ring depths and tile height.  The pass is HBM bound: the raw ring (TMA → transform) gets the
+// shared memory the other sections leave (~64 KB in flight per SM covers the loaded DRAM
+// latency).  Tiles of 256 points (two M=128 MMA blocks) halve every per-tile handshake per
+// point where they fit; the A ring (transform → MMA) then holds one tile per transform group.
+template <int MP, int KP, int TR>
+struct TcBudget {
+  static constexpr int a = TR == 256 ? 2 : 4;
   static constexpr int mw = (KP + 31) / 32;
-  static constexpr int raw_stride_max = ((kTileRows * MP * 4 + 256 + 1023) / 1024) * 1024;
-  static constexpr int fixed = a * kTileRows * 128 + 2 * KP * 128 +                      // A ring, B tile
+  static constexpr int raw_stride_max = ((TR * MP * 4 + 256 + 1023) / 1024) * 1024;
+  static constexpr int fixed = a * TR * 128 + 2 * KP * 128 +                          // A ring, B tile
                                ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024 +       // Δ accumulators
                                kQueueCap * (8 + 4 * mw) + 1024 +                       // recheck queue
                                2048 + 1024 + 8192;                                     // barriers, align, static
@@ -71,6 +74,13 @@ struct TcStages {
   static constexpr int fit_res = (227 * 1024 - fixed - cres) / raw_stride_max;
   static constexpr int fit = fit_res >= 4 ? fit_res : (227 * 1024 - fixed) / raw_stride_max;
   static constexpr int raw = fit > 12 ? 12 : fit;
+};
+template <int MP, int KP>
+struct TcStages {
+  static constexpr bool tall = false;  // 256-point tiles measured slower: one A buffer per group serializes transform and MMA
+  static constexpr int TR = tall ? 256 : 128;  // points per tile
+  static constexpr int raw = TcBudget<MP, KP, TR>::raw;
+  static constexpr int a = TcBudget<MP, KP, TR>::a;
   static_assert(raw >= 3, "shared-memory budget");
 };
 
@@ -107,6 +117,9 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// try_wait with a long suspend-time hint (10 ms, as CUTLASS's ClusterBarrier::wait): a waiting
+// thread sleeps until the phase completes instead of spinning, so waiting warps take no
+// issue slots from the warps doing the work (spinning waits were ~1/3 of all instructions)
 __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -116,21 +129,19 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       "selp.u32 %0, 1, 0, p;\n"
       "}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(64)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680)
       : "memory");
   return ok != 0;
 }
-// try_wait with a short suspend-time hint; bounded: a wait that cannot complete (a bug)
-// traps after ~8 s instead of hanging the device
+// bounded: a wait that cannot complete (a bug) traps instead of hanging the device
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if KM_WAIT_MODE == 1
   while (!mbar_test(bar, parity)) {
   }
 #else
-  if (mbar_try(bar, parity)) return;
-  const long long t0 = clock64();
+  uint32_t n = 0;
   while (!mbar_try(bar, parity)) {
-    if (clock64() - t0 > (1ll << 34)) __trap();
+    if (++n == (1u << 24)) __trap();
   }
 #endif
 }
@@ -277,10 +288,11 @@ struct TcLayout {
   static constexpr int KSTEPS = (2 * HW) / 16;       // kind::f16 MMA k-steps (16 halfs = 32 B each)
 };
 
-template <int KP>
+template <int KP, int MB>
 struct TcTmem {
-  static constexpr int NS = KP <= 32 ? 8 : KP <= 64 ? 4 : 2;  // TMEM score buffers (2KP columns each)
-  static constexpr uint32_t cols = NS * 2 * KP;
+  static constexpr int per = MB * 2 * KP;                                  // columns per tile
+  static constexpr int NS = 512 / per >= 8 ? 8 : 512 / per;                // TMEM score buffers
+  static constexpr uint32_t cols = NS * per;
   static constexpr uint32_t alloc = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
 };
 
@@ -292,9 +304,9 @@ struct TcSmem {
   // kres = k for the resident loop (two fp64 centre sets stay in shared memory), else 0
   __host__ __device__ TcSmem(int m, int kres) {
     // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
-    raw_stride = ((uint32_t)kTile * m * 4 + 256 + 1023) & ~1023u;
-    off_a = RS * raw_stride;                 // [AS][128 rows × 128 B]
-    off_w = off_a + AS * kTile * 128;        // [2KP rows × 128 B]
+    raw_stride = ((uint32_t)TcStages<MP, KP>::TR * m * 4 + 256 + 1023) & ~1023u;
+    off_a = RS * raw_stride;                 // [AS][TR rows × 128 B]
+    off_w = off_a + AS * TcStages<MP, KP>::TR * 128;  // [2KP rows × 128 B]
     off_acc = off_w + 2 * KP * 128;          // [KP·(MP+1) + KP] int64 Δ accumulators
     off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // recheck queue: rows, masks, scalars
     off_c = off_q + kQueueCap * (8 + 4 * ((KP + 31) / 32)) + 1024;  // [2][kres·m] fp64 centres (resident)
@@ -423,11 +435,13 @@ __device__ __forceinline__ int exact_candidates(const float* __restrict__ gx, in
 //   clusters (the host repairs them and relaunches).
 template <int MT, int KP, bool PRE>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
-  static_assert(kThreadsTC == 608, "warp-role layout");
+  static_assert(kThreadsTC == 640, "warp-role layout");
   constexpr int MP = MT > 0 ? MT : -MT;
   if (a.gate && (a.st->done || a.st->need_host)) return;
   using L = TcLayout<MP>;
-  using TM = TcTmem<KP>;
+  constexpr int TR = TcStages<MP, KP>::TR;  // points per tile
+  constexpr int MB = TR / 128;              // M=128 MMA blocks per tile
+  using TM = TcTmem<KP, MB>;
   const bool resident = a.resident != 0;
   const TcSmem<MP, KP> S(MT > 0 ? MT : a.m, resident ? a.k : 0);
   constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
@@ -457,7 +471,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   const int k = a.k;
   const int km = k * m;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  const int64_t ntiles = (a.n + TR - 1) / TR;
   // contiguous tile range per CTA: [t_lo, t_lo + my_tiles) (TLB- and DRAM-page-friendly streams)
   const int64_t t_lo = ntiles * blockIdx.x / gridDim.x;
   const int my_tiles = (int)(ntiles * (blockIdx.x + 1) / gridDim.x - t_lo);
@@ -489,13 +503,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       *reinterpret_cast<uint4*>(s_w + sw128(r, q)) = *reinterpret_cast<const uint4*>(a.wop + (size_t)r * 64 + q * 8);
     }
     // A operand buffers zeroed once (chunks beyond the used width stay zero)
-    for (int i = tid; i < AS * kTile * 8; i += nthr)
+    for (int i = tid; i < AS * TR * 8; i += nthr)
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
+    for (int i = tid; i < kQueueCap; i += nthr) s_q[i] = 0;
     if (resident)
       for (int i = tid; i < km; i += nthr) s_cbuf[i] = a.c64[i];
     if (tid == 0) {
-      s_qn[0] = 0u;
+      s_qn[0] = s_qn[1] = s_qn[2] = 0u;
       s_cmax[0] = a.cmax[0];
     }
     fence_proxy_async();
@@ -523,16 +538,71 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   for (int it = 0;; ++it) {
     const double* C = resident ? s_cbuf + cb * km : a.c64;
     if (pst && it < 256 && blockIdx.x == 0) pst[it * 8 + 0] = globaltimer();
-    if (warp == kProducerWarp) {
+    if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2] = (long long)globaltimer();
+    // exact re-decision of queue entry q (thread per point, candidate centres only); Δ into s_acc
+    auto redecide = [&](unsigned int q, long long ent) {
+      const long long row = (ent >> 8) & ((1ll << 54) - 1);
+      const int old = (int)(ent & 0xff) - 1;
+      uint32_t mk[MW];
+#pragma unroll
+      for (int w = 0; w < MW; ++w) mk[w] = s_qm[q * MW + w];
+      float xq[MP];
+      const int bl = resident ? exact_candidates<MP, MW>(a.x + row * m, m, s_cbuf + cb * km, mk, xq)
+                              : exact_candidates<MP, MW>(a.x + row * m, m, a.c64, mk, xq);
+      if (bl != old) {
+        a.labels[row] = bl;
+        if (!full) atomicAdd(&st->changed, 1ull);
+#pragma unroll
+        for (int f = 0; f < MP; ++f) {
+          if (f < m) {
+            const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
+                                             : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
+            smem_add64(s_acc + (size_t)bl * m + f, (unsigned long long)v);
+            if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
+          }
+        }
+        smem_add64(s_acc + (size_t)km + bl, 1ull);
+        if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+      }
+      s_q[q] = 0;  // free for the next pass
+    };
+    if (warp == kRecheckWarp) {
+      // ===================== recheck warp: re-decides queued points while the pass streams =====================
+      unsigned int done = 0;
+      for (;;) {
+        const unsigned int avail = __shfl_sync(0xffffffffu, min(*reinterpret_cast<volatile unsigned int*>(s_qn), (unsigned int)kQueueCap), 0);
+        if (done < avail) {
+          const unsigned int q = done + lane;
+          if (q < avail) {
+            long long ent;
+            while ((ent = *reinterpret_cast<volatile long long*>(s_q + q)) == 0) {
+            }
+            __threadfence_block();
+            redecide(q, ent);
+          }
+          done = min(done + 32u, avail);
+        } else {
+          const unsigned int fin = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile unsigned int*>(s_qn + 1), 0);
+          if (fin >= (unsigned int)kEpiWarps) {
+            __threadfence_block();
+            const unsigned int av2 = __shfl_sync(0xffffffffu, min(*reinterpret_cast<volatile unsigned int*>(s_qn), (unsigned int)kQueueCap), 0);
+            if (av2 == done) break;
+          } else {
+            __nanosleep(256);
+          }
+        }
+      }
+      if (lane == 0) s_qn[2] = done;
+    } else if (warp == kProducerWarp) {
       // ===================== TMA producer: tile g → raw slot g % RS =====================
       if (lane == 0) {
         const uint64_t pol = l2_policy_evict_first();
         auto issue = [&](int g, int i) {
           const int s = g % RS;
           if (g >= RS) mbar_wait(empty_raw + s, ((g / RS) - 1) & 1);
-          const int64_t row0 = (t_lo + i) * kTile;
+          const int64_t row0 = (t_lo + i) * TR;
           const int64_t rem = a.n - row0;
-          const int rows = rem < kTile ? (int)rem : kTile;
+          const int rows = rem < TR ? (int)rem : TR;
           const uint32_t bytes = ((uint32_t)rows * m * 4u) & ~15u;
           mbar_arrive_expect_tx(full_raw + s, bytes);
           if (bytes)
@@ -551,7 +621,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform → uniform registers
       constexpr uint32_t idesc = idesc_f16(2 * KP);
       const uint64_t bdesc0 = make_desc(w0, 16, 1024);
-      for (int i = (mj - (g0 & 1)) & 1; i < my_tiles; i += kMmaWarps) {
+      for (int i = (mj - (g0 & 1)) & 1; i < my_tiles && !(a.dbg_flags & 4); i += kMmaWarps) {
         const int g = g0 + i;
         const int sa = g % AS, ss = g % TM::NS;
         long long* ms = (a.dbg_times != nullptr && blockIdx.x == 0 && i < 64 && lane == 0 && it == (resident ? 100 : 0))
@@ -562,12 +632,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         if (g >= TM::NS) mbar_wait(s_empty + ss, ((g / TM::NS) - 1) & 1);
         if (ms) ms[2] = clock64();
         tc_fence_after();
-        const uint64_t adesc0 = make_desc(a0 + sa * (kTile * 128), 16, 1024);
-        const uint32_t dcol = tm + ss * 2 * KP;
         if (elect_one()) {
 #pragma unroll
-          for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
-            mma_f16(dcol, adesc0 + 2 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+          for (int mb = 0; mb < MB; ++mb) {  // block mb: points 128·mb.. of the tile → columns mb·2KP..
+            const uint64_t adesc0 = make_desc(a0 + sa * (TR * 128) + mb * (128 * 128), 16, 1024);
+            const uint32_t dcol = tm + ss * TM::per + mb * 2 * KP;
+#pragma unroll
+            for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
+              mma_f16(dcol, adesc0 + 2 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+          }
           mma_commit(s_full + ss);   // scores ready
           mma_commit(a_empty + sa);  // A buffer consumed
         }
@@ -584,63 +657,73 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       for (int i = (tg - (g0 & 1)) & 1; i < my_tiles; i += kTransformGroups) {
         const int g = g0 + i;
         const int s = g % RS, sa = g % AS;
-        const int64_t row0 = (t_lo + i) * kTile;
+        const int64_t row0 = (t_lo + i) * TR;
         const int64_t rem = a.n - row0;
-        const int rows = rem < kTile ? (int)rem : kTile;
-        const bool active = p < rows;
+        const int rows = rem < TR ? (int)rem : TR;
         const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[0] = clock64();
         mbar_wait(full_raw + s, (g / RS) & 1);
         if (stamp) ts[1] = clock64();
-        const float* rs = raw + s * (S.raw_stride / 4);
-        float xs[L::HW];
-        if (rows == kTile) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
-          const float* xr = rs + p * m;
-#pragma unroll
-          for (int f = 0; f < L::HW; ++f) {
-            const float v = (f < MP) ? xr[f] : 0.f;
-            xs[f] = (f < m) ? (PRE ? v * pre : v) : 0.f;
-          }
-        } else {  // ragged last tile: bulk part + ≤ 3 trailing floats from global
-          const uint32_t bulk_elems = (((uint32_t)rows * m * 4u) & ~15u) >> 2;
-          for (int f = 0; f < L::HW; ++f) {
-            float v = 0.f;
-            if (f < MP && f < m && active) {
-              const uint32_t e = (uint32_t)p * m + f;
-              v = ((e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e));
-              if (PRE) v *= pre;
-            }
-            xs[f] = v;
-          }
+        if (a.dbg_flags & 4) {  // tuning only: measure the TMA stream alone
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty_raw + s);
+          continue;
         }
+        const float* rs = raw + s * (S.raw_stride / 4);
+        if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+        if (stamp) ts[7] = clock64();
+        unsigned char* s_a = sm + S.off_a + sa * (TR * 128);
 #pragma unroll
-        for (int f = 0; f < L::HW; ++f)
-          if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
-        uint32_t hw[L::HW / 2], lw[L::HW / 2];
+        for (int mb = 0; mb < MB; ++mb) {  // thread = points p and p + 128 (tall tiles)
+          const int pp = p + 128 * mb;
+          const bool active = pp < rows;
+          float xs[L::HW];
+          if (rows == TR) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
+            const float* xr = rs + pp * m;
 #pragma unroll
-        for (int q = 0; q < L::HW / 2; ++q) {
-          const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
-          const float2 hf = __half22float2(h2);
-          const __half2 l2 = __floats2half2_rn(xs[2 * q] - hf.x, xs[2 * q + 1] - hf.y);
-          hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
-          lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
+            for (int f = 0; f < L::HW; ++f) {
+              const float v = (f < MP) ? xr[f] : 0.f;
+              xs[f] = (f < m) ? (PRE ? v * pre : v) : 0.f;
+            }
+          } else {  // ragged last tile: bulk part + ≤ 3 trailing floats from global
+            const uint32_t bulk_elems = (((uint32_t)rows * m * 4u) & ~15u) >> 2;
+            for (int f = 0; f < L::HW; ++f) {
+              float v = 0.f;
+              if (f < MP && f < m && active) {
+                const uint32_t e = (uint32_t)pp * m + f;
+                v = ((e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e));
+                if (PRE) v *= pre;
+              }
+              xs[f] = v;
+            }
+          }
+#pragma unroll
+          for (int f = 0; f < L::HW; ++f)
+            if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
+          uint32_t hw[L::HW / 2], lw[L::HW / 2];
+#pragma unroll
+          for (int q = 0; q < L::HW / 2; ++q) {
+            const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
+            const float2 hf = __half22float2(h2);
+            const __half2 l2 = __floats2half2_rn(xs[2 * q] - hf.x, xs[2 * q + 1] - hf.y);
+            hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
+            lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
+          }
+          unsigned char* s_ab = s_a + mb * (128 * 128);
+#pragma unroll
+          for (int q = 0; q < L::HW / 8; ++q) {
+            *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)(q ^ key) << 4)) =
+                make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+            *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
+                make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+          }
         }
         // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
         // the TMA producer may refill it
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_raw + s);
-        if (stamp) ts[7] = clock64();
-        if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);
         if (stamp) ts[2] = clock64();
-        unsigned char* s_a = sm + S.off_a + sa * (kTile * 128);
-#pragma unroll
-        for (int q = 0; q < L::HW / 8; ++q) {
-          *reinterpret_cast<uint4*>(s_a + row_off + ((uint32_t)(q ^ key) << 4)) =
-              make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-          *reinterpret_cast<uint4*>(s_a + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
-              make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
-        }
         fence_proxy_async();
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full + sa);
@@ -660,122 +743,150 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const double scale_d = a.scale_d;
       const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0;
       unsigned int my_changed = 0, my_rechecked = 0;
-      auto prev_label = [&](int i) -> int {  // previous label of this thread's point in tile i (or -1)
+      auto prev_label = [&](int i, int mb) -> int {  // previous label of point p + 128·mb of tile i (or -1)
         if (full || i >= my_tiles) return -1;
-        const int64_t r = (t_lo + i) * kTile + p;
+        const int64_t r = (t_lo + i) * TR + 128 * mb + p;
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
       const int i0 = (e - (g0 & 1)) & 1;
-      int old_next = prev_label(i0);
-      for (int i = i0; i < my_tiles; i += kEpiGroups) {
+      int old_next[MB];
+#pragma unroll
+      for (int mb = 0; mb < MB; ++mb) old_next[mb] = prev_label(i0, mb);
+      for (int i = i0; i < my_tiles && !(a.dbg_flags & 4); i += kEpiGroups) {
         const int g = g0 + i;
         const int ss = g % TM::NS;
-        const int64_t row0 = (t_lo + i) * kTile;
+        const int64_t row0 = (t_lo + i) * TR;
         const int64_t rem = a.n - row0;
-        const int rows = rem < kTile ? (int)rem : kTile;
-        const bool active = p < rows;
-        const int old = old_next;
-        old_next = prev_label(i + kEpiGroups);  // prefetch one tile ahead (global latency off the critical path)
+        const int rows = rem < TR ? (int)rem : TR;
+        int olds[MB];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          olds[mb] = old_next[mb];
+          old_next[mb] = prev_label(i + kEpiGroups, mb);  // prefetch one tile ahead (latency off the critical path)
+        }
         const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[4] = clock64();
         mbar_wait(s_full + ss, (g / TM::NS) & 1);
         if (stamp) ts[5] = clock64();
         tc_fence_after();
-        // top-2 over the scores: per 16-column chunk a 4-level tree, then a running merge.
-        // (The filter's argmin tie order is irrelevant: a tie is never certified.)
-        float best = __int_as_float(0x7f800000), min2 = best;
-        int bi = 0;
-#pragma unroll
-        for (int c0 = 0; c0 < KP; c0 += 16) {
-          uint32_t r0[16], r1[16];
-          tmem_ld16(tmem + lane_base + ss * 2 * KP + c0, r0);
-          tmem_ld16(tmem + lane_base + ss * 2 * KP + KP + c0, r1);
-          tmem_ld_wait();
-          float v[16], s2[16];
-          int ix[16];
-#pragma unroll
-          for (int jj = 0; jj < 16; ++jj) {  // padded centres (c ≥ k) score +65504: never best or runner-up
-            v[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
-            s2[jj] = __int_as_float(0x7f800000);
-            ix[jj] = c0 + jj;
-          }
-          if (a.dbg_scores != nullptr && active) {
-#pragma unroll
-            for (int jj = 0; jj < 16; ++jj)
-              if (c0 + jj < k) a.dbg_scores[(row0 + p) * k + c0 + jj] = v[jj] * inv_pre2;
-          }
-#pragma unroll
-          for (int w = 1; w < 16; w <<= 1) {
-#pragma unroll
-            for (int jj = 0; jj < 16; jj += 2 * w) {
-              const bool rb = v[jj + w] < v[jj];
-              const float lo = rb ? v[jj + w] : v[jj], hi = rb ? v[jj] : v[jj + w];
-              s2[jj] = fminf(hi, fminf(s2[jj], s2[jj + w]));
-              ix[jj] = rb ? ix[jj + w] : ix[jj];
-              v[jj] = lo;
-            }
-          }
-          const bool rb = v[0] < best;
-          min2 = fminf(rb ? best : v[0], fminf(min2, s2[0]));
-          bi = rb ? ix[0] : bi;
-          best = rb ? v[0] : best;
+        if (a.dbg_flags & 32) {  // timing experiment only: no epilogue work (labels unchanged)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty + ss);
+          continue;
         }
-        const bool unc = active && (exact_only || !(min2 > best + E2));
-        if (__any_sync(0xffffffffu, unc)) {
-          // uncertified: only centres whose filter score lies within 2E of the best can be the
-          // reference's argmin (every other one is strictly farther) — collect them as a mask
-          // (second look at the scores) and queue the point for the exact re-decision
+        int bis[MB];
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          const int pp = p + 128 * mb;
+          const bool active = pp < rows;
+          const int old = olds[mb];
+          const uint32_t tcol = tmem + lane_base + ss * TM::per + mb * 2 * KP;
+          // Certification: best = min score, candidates = {c : score ≤ best + E2}; the point is
+          // certified iff the best is the only candidate (then it is the reference's argmin).
+          // One packed counter per point: +1 per candidate, + c·2^8 (the index sum = the
+          // argmin when there is one candidate).  KP ≤ 32: the scores stay in registers.
+          constexpr int NCH = KP / 16;
+          constexpr bool KEEP = KP <= 32;
+          float vk[KEEP ? KP : 16];
+          float best = __int_as_float(0x7f800000);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) {
+            uint32_t r0[16], r1[16];
+            tmem_ld16(tcol + ch * 16, r0);
+            tmem_ld16(tcol + KP + ch * 16, r1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {  // padded centres (c ≥ k) score +65504: never a candidate
+              const float v = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+              vk[KEEP ? ch * 16 + jj : jj] = v;
+            }
+            if (a.dbg_scores != nullptr && active) {
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj)
+                if (ch * 16 + jj < k) a.dbg_scores[(row0 + pp) * k + ch * 16 + jj] = vk[KEEP ? ch * 16 + jj : jj] * inv_pre2;
+            }
+            float m4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              m4[q] = fminf(fminf(vk[(KEEP ? ch * 16 : 0) + 4 * q], vk[(KEEP ? ch * 16 : 0) + 4 * q + 1]),
+                            fminf(vk[(KEEP ? ch * 16 : 0) + 4 * q + 2], vk[(KEEP ? ch * 16 : 0) + 4 * q + 3]));
+            best = fminf(best, fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3])));
+          }
           const float thr = exact_only ? __int_as_float(0x7f800000) : best + E2;
+          uint32_t cnt = 0;  // candidates | index sum << 8
           uint32_t mk[MW];
 #pragma unroll
           for (int w = 0; w < MW; ++w) mk[w] = 0u;
 #pragma unroll
-          for (int c0 = 0; c0 < KP; c0 += 16) {
-            uint32_t r0[16], r1[16];
-            tmem_ld16(tmem + lane_base + ss * 2 * KP + c0, r0);
-            tmem_ld16(tmem + lane_base + ss * 2 * KP + KP + c0, r1);
-            tmem_ld_wait();
+          for (int ch = 0; ch < NCH; ++ch) {
+            if (!KEEP) {
+              uint32_t r0[16], r1[16];
+              tmem_ld16(tcol + ch * 16, r0);
+              tmem_ld16(tcol + KP + ch * 16, r1);
+              tmem_ld_wait();
+#pragma unroll
+              for (int jj = 0; jj < 16; ++jj) vk[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+            }
             uint32_t bits = 0;
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj)
-              bits |= (__uint_as_float(r0[jj]) + __uint_as_float(r1[jj]) <= thr && c0 + jj < k) ? (1u << jj) : 0u;
-            mk[c0 >> 5] |= bits << (c0 & 31);
+            for (int jj = 0; jj < 16; ++jj) {
+              const bool cand = vk[KEEP ? ch * 16 + jj : jj] <= thr;
+              cnt += cand ? (1u + ((uint32_t)(ch * 16 + jj) << 8)) : 0u;
+              bits |= cand ? (1u << jj) : 0u;
+            }
+            mk[(ch * 16) >> 5] |= bits << ((ch * 16) & 31);
           }
-          if (unc) {
-            ++my_rechecked;
-            const unsigned int slot = atomicAdd(s_qn, 1u);
-            if (slot < kQueueCap) {
-              s_q[slot] = ((row0 + p) << 8) | (long long)(old + 1);  // row | previous label + 1 (0 = none)
-              const float* gr = a.x + (row0 + p) * m;  // keep the row in L2 until the tail reads it
-              prefetch_l2_keep(gr);
-              prefetch_l2_keep(gr + m - 1);
+          int bi = (int)(cnt >> 8);
+          const bool unc = active && (cnt & 0xff) != 1u;
+          if (__any_sync(0xffffffffu, unc)) {
+            if (unc) {
+              // uncertified: only the candidates can be the reference's argmin (every other
+              // centre is strictly farther) — queue the point with its candidate mask
+              ++my_rechecked;
+              const unsigned int slot = atomicAdd(s_qn, 1u);
+              if (slot < kQueueCap) {
+                const float* gr = a.x + (row0 + pp) * m;  // keep the row in L2 until it is re-decided
+                prefetch_l2_keep(gr);
+                prefetch_l2_keep(gr + m - 1);
 #pragma unroll
-              for (int w = 0; w < MW; ++w) s_qm[slot * MW + w] = mk[w];
-              bi = old;  // decided in the tail
-            } else {     // staging full (rare): decide here
-              float xq[MP];
-              bi = exact_candidates<MP, MW>(a.x + (row0 + p) * m, m, C, mk, xq);
+                for (int w = 0; w < MW; ++w) s_qm[slot * MW + w] = mk[w];
+                __threadfence_block();  // masks before the entry that publishes them
+                // flag | row | previous label + 1 (0 = none); an entry of 0 = not yet written
+                *reinterpret_cast<volatile long long*>(s_q + slot) =
+                    kQueueFlag | ((row0 + pp) << 8) | (long long)(old + 1);
+                bi = old;  // decided by the recheck warp (or the tail)
+              } else {     // staging full (rare): decide here
+                float xq[MP];
+                bi = exact_candidates<MP, MW>(a.x + (row0 + pp) * m, m, C, mk, xq);
+              }
             }
           }
+          bis[mb] = active ? bi : old;
         }
         tc_fence_before();  // TMEM reads ordered before the MMA reuses this buffer
         __syncwarp();
         if (lane == 0) mbar_arrive(s_empty + ss);
-        if (active && bi != old) {
-          // --- exact incremental update of the per-cluster fixed-point sums
-          ++my_changed;
-          a.labels[row0 + p] = bi;
-          const float* xr = a.x + (row0 + p) * m;  // just streamed: L2 hit
-          for (int f = 0; f < m; ++f) {
-            const float xv = __ldg(xr + f);
-            const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d))
-                                           : __float2ll_rn(__fmul_rn(xv, scale_f));
-            smem_add64(s_acc + (size_t)bi * m + f, (unsigned long long)v);
-            if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          const int bi = bis[mb], old = olds[mb];
+          if (bi != old) {
+            // --- exact incremental update of the per-cluster fixed-point sums
+            const int64_t row = row0 + 128 * mb + p;
+            ++my_changed;
+            a.labels[row] = bi;
+            const float* xr = a.x + row * m;  // just streamed: L2 hit
+            for (int f = 0; f < m; ++f) {
+              const float xv = __ldg(xr + f);
+              const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d))
+                                             : __float2ll_rn(__fmul_rn(xv, scale_f));
+              smem_add64(s_acc + (size_t)bi * m + f, (unsigned long long)v);
+              if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
+            }
+            smem_add64(s_acc + (size_t)km + bi, 1ull);
+            if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
           }
-          smem_add64(s_acc + (size_t)km + bi, 1ull);
-          if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
         }
         if (stamp) ts[6] = clock64();
       }
@@ -787,48 +898,27 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       }
       if (lane == 0 && w2) atomicAdd(&st->changed, (unsigned long long)w2);
       if (lane == 0 && w3) atomicAdd(&st->rechecked, (unsigned long long)w3);
+      __threadfence_block();
+      __syncwarp();
+      if (lane == 0) atomicAdd(s_qn + 1, 1u);  // this epilogue warp has queued everything of the pass
     }
     // ===================== tail (all warps) =====================
     tc_fence_before();
     __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
+    if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2 + 1] = (long long)globaltimer();
     double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
     const int stage_cap = (int)(RS * S.raw_stride / 8);
     {
-      // exact re-decision of the queued points: thread per point over its candidate centres
+      // queue entries the recheck warp had not reached when the pass ended: thread per point
       const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
-      for (unsigned int q = tid; q < qn; q += kThreadsTC) {
-        const long long ent = s_q[q];
-        const long long row = ent >> 8;
-        const int old = (int)(ent & 0xff) - 1;
-        uint32_t mk[MW];
-#pragma unroll
-        for (int w = 0; w < MW; ++w) mk[w] = s_qm[q * MW + w];
-        long long* qs = (a.dbg_times != nullptr && blockIdx.x < 4 && it == 100 && q < 64)
-                            ? a.dbg_times + 6144 + (blockIdx.x * 64 + q) * 4 : nullptr;
-        if (qs) qs[0] = clock64();
-        float xq[MP];
-        const int bl = resident ? exact_candidates<MP, MW>(a.x + row * m, m, s_cbuf + cb * km, mk, xq, qs ? qs + 2 : nullptr)
-                                : exact_candidates<MP, MW>(a.x + row * m, m, a.c64, mk, xq);
-        if (qs) { qs[1] = clock64() + (bl == 12345); qs[3] = __popc(mk[0]) + 100 * (bl != old); }
-        if (bl != old) {
-          a.labels[row] = bl;
-          if (!full) atomicAdd(&st->changed, 1ull);
-#pragma unroll
-          for (int f = 0; f < MP; ++f) {
-            if (f < m) {
-              const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
-                                               : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
-              smem_add64(s_acc + (size_t)bl * m + f, (unsigned long long)v);
-              if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
-            }
-          }
-          smem_add64(s_acc + (size_t)km + bl, 1ull);
-          if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
-        }
-      }
+      for (unsigned int q = s_qn[2] + tid; q < qn; q += kThreadsTC) redecide(q, s_q[q]);
       __syncthreads();
-      if (tid == 0) s_qn[0] = 0u;
+      if (tid == 0) {
+        s_qn[0] = 0u;
+        s_qn[1] = 0u;
+        s_qn[2] = 0u;
+      }
       if (pst && it < 256) atomicMax(pst + it * 8 + 2, globaltimer());
     }
     if (!resident) {
@@ -967,7 +1057,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           st->need_host = 1;
         }
         stop = true;
-      } else if (!(flags & 2)) {
+      } else if (!(flags & 2) && !(a.dbg_flags & 64)) {  // (dbg 64: timing experiments never converge)
         if (pub && tid == 0) {
           st->n_empty = 0;
           st->converged = 1;
@@ -1015,6 +1105,7 @@ inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_
   cudaError_t c = cudaFuncGetAttributes(&fa, kern);
   if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncGetAttributes(tc)"); return 1; }
   const size_t smem = TcSmem<MP, KP>(a.m, a.resident ? a.k : 0).total;
+  (void)MP;
   if (smem + fa.sharedSizeBytes > smem_optin) {
     snprintf(msg, len, "tensor-core pass needs %zu B of shared memory (max %zu)", smem + fa.sharedSizeBytes,
              smem_optin);
@@ -1028,7 +1119,7 @@ inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_
   c = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsTC, smem);
   if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "occupancy(tc)"); return 1; }
   if (per_sm < 1) { snprintf(msg, len, "tensor-core pass does not fit on an SM"); return 2; }
-  const int64_t ntiles = (a.n + kTile - 1) / kTile;
+  const int64_t ntiles = (a.n + TcStages<MP, KP>::TR - 1) / TcStages<MP, KP>::TR;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));  // one persistent CTA/SM
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
