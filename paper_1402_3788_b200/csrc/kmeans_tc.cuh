@@ -101,6 +101,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 // Wait strategy (build-time tuning knob):
 //   KM_WAIT_MODE 1: mbarrier.test_wait polling
 //   otherwise     : mbarrier.try_wait with a short suspend-time hint (bounded)
+// Tuning instrumentation (per-tile clock stamps, timing experiments) is compiled in only for
+// the KM_TC_TUNING=1 library variant (tools/); the product kernel carries none of it.
+#ifndef KM_TC_TUNING
+#define KM_TC_TUNING 0
+#endif
+#define KM_DBG_FLAGS (KM_TC_TUNING ? a.dbg_flags : 0)
 #ifndef KM_WAIT_MODE
 #define KM_WAIT_MODE 2
 #endif
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   int issued = 0;  // producer: tiles of the current pass already in flight
 
   // tuning only: per-pass phase ends (globaltimer, max over CTAs) of the resident loop
-  unsigned long long* pst = (a.dbg_times != nullptr && resident && tid == 0)
+  unsigned long long* pst = (KM_TC_TUNING && a.dbg_times != nullptr && resident && tid == 0)
                                 ? reinterpret_cast<unsigned long long*>(a.dbg_times + 4096) : nullptr;
   for (int it = 0;; ++it) {
     const double* C = resident ? s_cbuf + cb * km : a.c64;
@@ -621,10 +627,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform → uniform registers
       constexpr uint32_t idesc = idesc_f16(2 * KP);
       const uint64_t bdesc0 = make_desc(w0, 16, 1024);
-      for (int i = (mj - (g0 & 1)) & 1; i < my_tiles && !(a.dbg_flags & 4); i += kMmaWarps) {
+      for (int i = (mj - (g0 & 1)) & 1; i < my_tiles && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
         const int g = g0 + i;
         const int sa = g % AS, ss = g % TM::NS;
-        long long* ms = (a.dbg_times != nullptr && blockIdx.x == 0 && i < 64 && lane == 0 && it == (resident ? 100 : 0))
+        long long* ms = (KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && i < 64 && lane == 0 && it == (resident ? 100 : 0))
                             ? a.dbg_times + 3072 + i * 4 : nullptr;
         if (ms) ms[0] = clock64();
         mbar_wait(a_full + sa, (g / AS) & 1);
@@ -660,12 +666,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const int64_t row0 = (t_lo + i) * TR;
         const int64_t rem = a.n - row0;
         const int rows = rem < TR ? (int)rem : TR;
-        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
+        const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[0] = clock64();
         mbar_wait(full_raw + s, (g / RS) & 1);
         if (stamp) ts[1] = clock64();
-        if (a.dbg_flags & 4) {  // tuning only: measure the TMA stream alone
+        if (KM_DBG_FLAGS & 4) {  // tuning only: measure the TMA stream alone
           __syncwarp();
           if (lane == 0) mbar_arrive(empty_raw + s);
           continue;
@@ -745,6 +751,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       unsigned int my_changed = 0, my_rechecked = 0;
       auto prev_label = [&](int i, int mb) -> int {  // previous label of point p + 128·mb of tile i (or -1)
         if (full || i >= my_tiles) return -1;
+        if (KM_DBG_FLAGS & 128) return 0;  // timing experiment only: no label loads
         const int64_t r = (t_lo + i) * TR + 128 * mb + p;
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
@@ -752,7 +759,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       int old_next[MB];
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb) old_next[mb] = prev_label(i0, mb);
-      for (int i = i0; i < my_tiles && !(a.dbg_flags & 4); i += kEpiGroups) {
+      for (int i = i0; i < my_tiles && !(KM_DBG_FLAGS & 4); i += kEpiGroups) {
         const int g = g0 + i;
         const int ss = g % TM::NS;
         const int64_t row0 = (t_lo + i) * TR;
@@ -764,13 +771,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           olds[mb] = old_next[mb];
           old_next[mb] = prev_label(i + kEpiGroups, mb);  // prefetch one tile ahead (latency off the critical path)
         }
-        const bool stamp = a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
+        const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[4] = clock64();
         mbar_wait(s_full + ss, (g / TM::NS) & 1);
         if (stamp) ts[5] = clock64();
         tc_fence_after();
-        if (a.dbg_flags & 32) {  // timing experiment only: no epilogue work (labels unchanged)
+        if (KM_DBG_FLAGS & 32) {  // timing experiment only: no epilogue work (labels unchanged)
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(s_empty + ss);
@@ -839,7 +846,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             mk[(ch * 16) >> 5] |= bits << ((ch * 16) & 31);
           }
           int bi = (int)(cnt >> 8);
-          const bool unc = active && (cnt & 0xff) != 1u;
+          const bool unc = active && (cnt & 0xff) != 1u && !(KM_DBG_FLAGS & 256);  // (dbg 256: timing only)
           if (__any_sync(0xffffffffu, unc)) {
             if (unc) {
               // uncertified: only the candidates can be the reference's argmin (every other
@@ -1057,7 +1064,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           st->need_host = 1;
         }
         stop = true;
-      } else if (!(flags & 2) && !(a.dbg_flags & 64)) {  // (dbg 64: timing experiments never converge)
+      } else if (!(flags & 2) && !(KM_DBG_FLAGS & 64)) {  // (dbg 64: timing experiments never converge)
         if (pub && tid == 0) {
           st->n_empty = 0;
           st->converged = 1;
