@@ -304,8 +304,8 @@ def run_ours(args, cfg_name):
     alg_bytes = n * (4 * m + 4)  # points read once (fp32) + int32 labels written once
     achieved = alg_bytes / (pass_ms * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_from_profiles(cfg_name), "kernel": "lloyd_pass_kernel",
-                "kernel_ms": pass_ms, "alg_bytes_per_launch": alg_bytes, "peak_kind": peak_kind,
+                "traffic": traffic_from_profiles(cfg_name), "kernel": "lloyd_pass_tc_kernel (resident loop; per-pass time = launch time / passes)",
+                "kernel_ms_per_pass": pass_ms, "alg_bytes_per_pass": alg_bytes, "peak_kind": peak_kind,
                 "pass_share_of_step": pass_ms / ms_per_step}
 
     # e2e: the public API from pinned host buffers, full fit to convergence
