@@ -35,6 +35,10 @@ struct km_engine {
   // resident points
   void* x = nullptr;
   bool x_owned = false;
+  // grow-only device buffers (a reload / a new k reuses them when large enough; freed at destroy)
+  void* xbuf = nullptr;             // owned points (fp32, or fp64 when narrowing would lose bits)
+  void* stage = nullptr;            // fp64 upload staging
+  size_t xbuf_cap = 0, stage_cap = 0, labels_cap = 0, rr_cap = 0, d2_cap = 0, l64_cap = 0, partials_cap = 0;
   int64_t n = 0;
   int32_t m = 0;
   int32_t point_bytes = 4;
@@ -129,6 +133,21 @@ static int dalloc(km_engine* e, P** p, size_t bytes) {
 }
 
 static void dfree(void* p) { if (p) cudaFree(p); }
+
+static int grow(km_engine* e, void** p, size_t* cap, size_t bytes) {
+  if (*p && *cap >= bytes) return KM_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  cudaError_t c = cudaMalloc(p, bytes ? bytes : 16);
+  if (c != cudaSuccess) { *p = nullptr; return cuda_fail(e, c, "cudaMalloc"); }
+  *cap = bytes;
+  return KM_OK;
+}
+template <typename P>
+static int grow(km_engine* e, P** p, size_t* cap, size_t bytes) {
+  return grow(e, reinterpret_cast<void**>(p), cap, bytes);
+}
 
 // ---------------------------------------------------------------------------
 // launch helpers
@@ -474,15 +493,17 @@ static int grid_for(km_engine* e, int64_t n, int per_sm = 8) {
 // ---------------------------------------------------------------------------
 // buffers
 // ---------------------------------------------------------------------------
+// k-sized buffers only; the n-sized ones (labels, recheck queue, d2, label staging, partials) are
+// grow-only and live until destroy
 static void free_k(km_engine* e) {
-  dfree(e->labels); dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
-  dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->d2); dfree(e->partials); dfree(e->winner);
-  dfree(e->scratch_d); dfree(e->labels64); dfree(e->wop); dfree(e->tot); dfree(e->recheck_rows);
+  dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
+  dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->winner);
+  dfree(e->scratch_d); dfree(e->wop); dfree(e->tot);
   dfree(e->recheck_count); dfree(e->cta_done); dfree(e->grid_sync);
-  e->labels = nullptr; e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
-  e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->d2 = nullptr; e->partials = nullptr; e->winner = nullptr;
-  e->scratch_d = nullptr; e->labels64 = nullptr; e->wop = nullptr; e->tot = nullptr;
-  e->recheck_rows = nullptr; e->recheck_count = nullptr; e->cta_done = nullptr; e->grid_sync = nullptr;
+  e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
+  e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->winner = nullptr;
+  e->scratch_d = nullptr; e->wop = nullptr; e->tot = nullptr;
+  e->recheck_count = nullptr; e->cta_done = nullptr; e->grid_sync = nullptr;
   e->resident_unfit = false;
   e->k = 0;
   e->kp = 0;
@@ -496,7 +517,7 @@ static int ensure_k(km_engine* e, int32_t k) {
   const int m = e->m;
   e->mpad = mp_for(m) ? mp_for(m) : ((m + 3) & ~3);
   int r;
-  if ((r = dalloc(e, &e->labels, sizeof(int32_t) * (size_t)e->n))) return r;
+  if ((r = grow(e, &e->labels, &e->labels_cap, sizeof(int32_t) * (size_t)e->n))) return r;
   if ((r = dalloc(e, &e->part, 8 * ((size_t)k * m + k)))) return r;
   if ((r = dalloc(e, &e->cur, 8 * (size_t)k * m))) return r;
   if ((r = dalloc(e, &e->prev, 8 * (size_t)k * m))) return r;
@@ -506,13 +527,13 @@ static int ensure_k(km_engine* e, int32_t k) {
   if ((r = dalloc(e, &e->cmax, 16))) return r;
   if ((r = dalloc(e, &e->scratch_d, 8 * 2 * (size_t)k * m))) return r;
   e->n_partials = grid_for(e, e->n);
-  if ((r = dalloc(e, &e->partials, sizeof(ArgMax) * (size_t)e->n_partials))) return r;
+  if ((r = grow(e, &e->partials, &e->partials_cap, sizeof(ArgMax) * (size_t)e->n_partials))) return r;
   if ((r = dalloc(e, &e->winner, sizeof(ArgMax)))) return r;
   e->kp = k <= 64 ? ((k + 15) & ~15) : ((k + 31) & ~31);
   if ((r = dalloc(e, &e->wop, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp))) return r;
   CK(cudaMemsetAsync(e->wop, 0, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp, e->stream));
   if ((r = dalloc(e, &e->tot, 8 * ((size_t)k * m + k)))) return r;
-  if ((r = dalloc(e, &e->recheck_rows, 8 * (size_t)e->n))) return r;
+  if ((r = grow(e, &e->recheck_rows, &e->rr_cap, 8 * (size_t)e->n))) return r;
   if ((r = dalloc(e, &e->recheck_count, 16))) return r;
   CK(cudaMemsetAsync(e->recheck_count, 0, 16, e->stream));
   if ((r = dalloc(e, &e->cta_done, 16))) return r;
@@ -595,8 +616,7 @@ static int after_points_loaded(km_engine* e) {
 
 static int drop_points(km_engine* e) {
   free_k(e);
-  if (e->x && e->x_owned) cudaFree(e->x);
-  e->x = nullptr;
+  e->x = nullptr;  // an owned copy lives on in xbuf / stage for the next load
   e->x_owned = false;
   e->n = 0;
   e->m = 0;
@@ -615,7 +635,7 @@ static int validate_points_shape(km_engine* e, const void* x, int64_t n, int32_t
 // repair (engine.py:265-276), single shard
 // ---------------------------------------------------------------------------
 static int self_d2(km_engine* e) {
-  if (!e->d2) { int r = dalloc(e, &e->d2, 8 * (size_t)e->n); if (r) return r; }
+  { int r = grow(e, &e->d2, &e->d2_cap, 8 * (size_t)e->n); if (r) return r; }
   const int g = grid_for(e, e->n);
   if (e->point_bytes == 4)
     self_d2_kernel<float><<<g, 256, 0, e->stream>>>((const float*)e->x, e->n, e->m, e->cur, e->labels, e->d2);
@@ -660,7 +680,7 @@ static int repair_local(km_engine* e) {
 }
 
 static int download_labels(km_engine* e, int64_t* out) {
-  if (!e->labels64) { int r = dalloc(e, &e->labels64, 8 * (size_t)e->n); if (r) return r; }
+  { int r = grow(e, &e->labels64, &e->l64_cap, 8 * (size_t)e->n); if (r) return r; }
   widen_labels_kernel<<<grid_for(e, e->n), 256, 0, e->stream>>>(e->labels, e->n, e->labels64);
   CK_LAUNCH("widen_labels_kernel");
   e->stats.kernel_launches += 1;
@@ -734,6 +754,8 @@ int km_destroy(km_engine* e) {
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
   drop_points(e);
+  dfree(e->xbuf); dfree(e->stage); dfree(e->labels); dfree(e->recheck_rows); dfree(e->d2);
+  dfree(e->labels64); dfree(e->partials);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   dfree(e->st);
   dfree(e->scratch_u);
@@ -769,8 +791,8 @@ int km_load_points_f32(km_engine* e, const float* x, int64_t n, int32_t m) {
   if (r) return r;
   cudaSetDevice(e->device);
   drop_points(e);
-  void* d = nullptr;
-  if ((r = dalloc(e, &d, sizeof(float) * (size_t)n * m))) return r;
+  if ((r = grow(e, &e->xbuf, &e->xbuf_cap, sizeof(float) * (size_t)n * m))) return r;
+  void* d = e->xbuf;
   e->x = d;
   e->x_owned = true;
   e->n = n;
@@ -789,22 +811,18 @@ int km_load_points_f64(km_engine* e, const double* x, int64_t n, int32_t m) {
   cudaSetDevice(e->device);
   const int64_t count = n * (int64_t)m;
   drop_points(e);
-  void* d64 = nullptr;
-  if ((r = dalloc(e, &d64, sizeof(double) * (size_t)count))) return r;
+  if ((r = grow(e, &e->stage, &e->stage_cap, sizeof(double) * (size_t)count))) return r;
+  void* d64 = e->stage;
   CK(cudaMemcpyAsync(d64, x, sizeof(double) * (size_t)count, cudaMemcpyHostToDevice, e->stream));
   int flags[2] = {0, 0};
-  if ((r = scan_points(e, d64, 8, count, flags))) { cudaFree(d64); return r; }
-  if (flags[0]) { cudaFree(d64); return set_err(e, KM_ERR_CONTRACT, "coords contains NaN or infinite values"); }
+  if ((r = scan_points(e, d64, 8, count, flags))) return r;
+  if (flags[0]) return set_err(e, KM_ERR_CONTRACT, "coords contains NaN or infinite values");
   if (!flags[1]) {  // lossless: keep the fp32 copy only (half the bytes per pass)
-    void* d32 = nullptr;
-    if ((r = dalloc(e, &d32, sizeof(float) * (size_t)count))) { cudaFree(d64); return r; }
-    narrow_f64_kernel<<<grid_for(e, count, 4), 256, 0, e->stream>>>((const double*)d64, count, (float*)d32);
-    cudaError_t c = cudaGetLastError();
-    if (c == cudaSuccess) c = cudaStreamSynchronize(e->stream);
-    cudaFree(d64);
-    if (c != cudaSuccess) { cudaFree(d32); return cuda_fail(e, c, "narrow_f64_kernel"); }
+    if ((r = grow(e, &e->xbuf, &e->xbuf_cap, sizeof(float) * (size_t)count))) return r;
+    narrow_f64_kernel<<<grid_for(e, count, 4), 256, 0, e->stream>>>((const double*)d64, count, (float*)e->xbuf);
+    CK_LAUNCH("narrow_f64_kernel");
     e->stats.kernel_launches += 1;
-    e->x = d32;
+    e->x = e->xbuf;
     e->point_bytes = 4;
   } else {
     e->x = d64;
