@@ -78,7 +78,8 @@ struct km_engine {
   long long* recheck_rows = nullptr;     // queue of uncertified points (n)
   unsigned int* recheck_count = nullptr;
   unsigned int* cta_done = nullptr;      // fused-finish completion counter
-  unsigned int* grid_sync = nullptr;     // resident loop: barrier arrivals, totals consumed
+  unsigned int* grid_sync = nullptr;     // resident loop: barrier arrivals
+  unsigned long long* dlt = nullptr;     // resident loop: [3][k·m + k] per-pass deltas
   bool resident_unfit = false;           // the resident TC loop does not fit this shape (use per-iteration launches)
   bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
   int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required
@@ -267,7 +268,11 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   a.fin.full = full ? 1 : 0;
   a.resident = resident ? 1 : 0;
   a.grid_sync = e->grid_sync;
-  if (resident) CK(cudaMemsetAsync(e->grid_sync, 0, 16, e->stream));
+  a.dlt = e->dlt;
+  if (resident) {
+    CK(cudaMemsetAsync(e->grid_sync, 0, 16, e->stream));
+    CK(cudaMemsetAsync(e->dlt, 0, 3 * 8 * ((size_t)e->k * e->m + e->k), e->stream));
+  }
   a.st = e->st;
   a.gate = gated ? 1 : 0;
   a.dbg_scores = e->dbg_scores;
@@ -499,7 +504,8 @@ static void free_k(km_engine* e) {
   dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
   dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->winner);
   dfree(e->scratch_d); dfree(e->wop); dfree(e->tot);
-  dfree(e->recheck_count); dfree(e->cta_done); dfree(e->grid_sync);
+  dfree(e->recheck_count); dfree(e->cta_done); dfree(e->grid_sync); dfree(e->dlt);
+  e->dlt = nullptr;
   e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
   e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->winner = nullptr;
   e->scratch_d = nullptr; e->wop = nullptr; e->tot = nullptr;
@@ -538,6 +544,7 @@ static int ensure_k(km_engine* e, int32_t k) {
   CK(cudaMemsetAsync(e->recheck_count, 0, 16, e->stream));
   if ((r = dalloc(e, &e->cta_done, 16))) return r;
   if ((r = dalloc(e, &e->grid_sync, 16))) return r;
+  if ((r = dalloc(e, &e->dlt, 3 * 8 * ((size_t)k * m + k)))) return r;
   CK(cudaMemsetAsync(e->cta_done, 0, 16, e->stream));
   CK(cudaMemsetAsync(e->tot, 0, 8 * ((size_t)k * m + k), e->stream));
   e->next_full = true;

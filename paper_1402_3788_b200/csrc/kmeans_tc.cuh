@@ -61,14 +61,14 @@ constexpr int kThreadsTC = (kRecheckWarp + 1) * 32;
 // point where they fit; the A ring (transform → MMA) then holds one tile per transform group.
 template <int MP, int KP, int TR>
 struct TcBudget {
-  static constexpr int a = TR == 256 ? 2 : 4;
+  static constexpr int a = 4;  // two A buffers per transform group
   static constexpr int mw = (KP + 31) / 32;
   static constexpr int raw_stride_max = ((TR * MP * 4 + 256 + 1023) / 1024) * 1024;
   static constexpr int fixed = a * TR * 128 + 2 * KP * 128 +                          // A ring, B tile
                                ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024 +       // Δ accumulators
                                kQueueCap * (8 + 4 * mw) + 1024 +                       // recheck queue
                                2048 + 1024 + 8192;                                     // barriers, align, static
-  static constexpr int cres = ((2 * KP * MP * 8) + 1023) / 1024 * 1024;                // resident centres
+  static constexpr int cres = ((3 * KP * MP + KP) * 8 + 1023) / 1024 * 1024;          // resident centres + totals
   // keep room for the resident loop's centres unless that would starve the raw ring
   // (the widest shapes then run launch-per-iteration)
   static constexpr int fit_res = (227 * 1024 - fixed - cres) / raw_stride_max;
@@ -77,11 +77,21 @@ struct TcBudget {
 };
 template <int MP, int KP>
 struct TcStages {
-  static constexpr bool tall = false;  // 256-point tiles measured slower: one A buffer per group serializes transform and MMA
+#ifndef KM_TALL_TILES
+#define KM_TALL_TILES 0
+#endif
+  // 256-point tiles (two M=128 MMA blocks per tile: half the handshakes per point) when at least
+  // two 256-row raw slots (≥ 50 KB in flight) fit beside the doubled A ring and the resident state
+  static constexpr bool tall = KM_TALL_TILES && KP <= 32 &&
+                               (227 * 1024 - TcBudget<MP, KP, 256>::fixed - TcBudget<MP, KP, 256>::cres) /
+                                       TcBudget<MP, KP, 256>::raw_stride_max >= 2;
   static constexpr int TR = tall ? 256 : 128;  // points per tile
-  static constexpr int raw = TcBudget<MP, KP, TR>::raw;
-  static constexpr int a = TcBudget<MP, KP, TR>::a;
-  static_assert(raw >= 3, "shared-memory budget");
+  static constexpr int raw_fit = tall ? (227 * 1024 - TcBudget<MP, KP, 256>::fixed - TcBudget<MP, KP, 256>::cres) /
+                                            TcBudget<MP, KP, 256>::raw_stride_max
+                                      : TcBudget<MP, KP, 128>::raw;
+  static constexpr int raw = raw_fit > 12 ? 12 : raw_fit;
+  static constexpr int a = 4;
+  static_assert(raw >= 2, "shared-memory budget");
 };
 
 // ---- PTX helpers -----------------------------------------------------------
@@ -306,18 +316,21 @@ struct TcTmem {
 template <int MP, int KP>
 struct TcSmem {
   static constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
-  uint32_t raw_stride, off_raw = 0, off_a, off_w, off_acc, off_q, off_c, off_bar, total;
+  uint32_t raw_stride, off_raw, off_a, off_w, off_acc, off_q, off_c, off_bar, total;
   // kres = k for the resident loop (two fp64 centre sets stay in shared memory), else 0
   __host__ __device__ TcSmem(int m, int kres) {
+    // fixed-size sections first (compile-time offsets: no per-use address arithmetic in the
+    // hot loops), then the raw ring (row stride depends on m) and the resident centres (on k)
+    off_bar = 0;                              // mbarriers + TMEM address (1 KiB)
+    off_w = 1024;                             // [2KP rows × 128 B] B operand (SW128)
+    off_a = off_w + 2 * KP * 128;             // [AS][TR rows × 128 B]
+    off_acc = off_a + AS * TcStages<MP, KP>::TR * 128;                    // [KP·(MP+1) + KP] int64 Δ
+    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;    // recheck queue: rows, masks, scalars
+    off_raw = off_q + ((kQueueCap * (8 + 4 * ((KP + 31) / 32)) + 1024) + 1023) / 1024 * 1024;
     // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
     raw_stride = ((uint32_t)TcStages<MP, KP>::TR * m * 4 + 256 + 1023) & ~1023u;
-    off_a = RS * raw_stride;                 // [AS][TR rows × 128 B]
-    off_w = off_a + AS * TcStages<MP, KP>::TR * 128;  // [2KP rows × 128 B]
-    off_acc = off_w + 2 * KP * 128;          // [KP·(MP+1) + KP] int64 Δ accumulators
-    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // recheck queue: rows, masks, scalars
-    off_c = off_q + kQueueCap * (8 + 4 * ((KP + 31) / 32)) + 1024;  // [2][kres·m] fp64 centres (resident)
-    off_bar = off_c + ((uint32_t)(2 * kres * m * 8) + 1023) / 1024 * 1024;
-    total = off_bar + 1024 + 1024;           // barriers + 1 KiB alignment slack
+    off_c = off_raw + RS * raw_stride;        // resident: [2][kres·m] fp64 centres, then [kres·m + kres] int64 totals
+    total = off_c + ((uint32_t)((2 * kres * m + kres * m + kres) * 8) + 1023) / 1024 * 1024 + 1024;  // + 1 KiB slack
   }
 };
 
@@ -464,6 +477,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   unsigned int* s_qn = s_qm + kQueueCap * MW;                                  // [0] queue length
   float* s_cmax = reinterpret_cast<float*>(s_qn + 4);                          // resident: max ‖c‖
   double* s_cbuf = reinterpret_cast<double*>(sm + S.off_c);                            // resident: [2][k·m]
+  unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(s_cbuf + 2 * (size_t)a.k * (MT > 0 ? MT : a.m));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S.off_bar);
   uint64_t* full_raw = bars;                 // [RS] TMA → transform
   uint64_t* empty_raw = full_raw + RS;       // [RS] transform → TMA
@@ -513,8 +527,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
     for (int i = tid; i < kQueueCap; i += nthr) s_q[i] = 0;
-    if (resident)
+    if (resident) {
       for (int i = tid; i < km; i += nthr) s_cbuf[i] = a.c64[i];
+      for (int i = tid; i < nacc; i += nthr) s_tot[i] = a.fin.tot[i];  // totals of the current labels
+    }
     if (tid == 0) {
       s_qn[0] = s_qn[1] = s_qn[2] = 0u;
       s_cmax[0] = a.cmax[0];
@@ -948,15 +964,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       }
       break;
     }
-    // ---- resident: Δ → running totals, grid barrier ----
-    // the totals of the previous pass must have been read by every CTA before they move again
-    if (tid == 0) grid_spin(a.grid_sync + 1, (unsigned int)it * gridDim.x);
-    __syncthreads();
-    unsigned long long* tot = a.fin.tot;
+    // ---- resident: Δ → the pass's global delta buffer, grid barrier ----
+    // Three delta buffers rotate: pass it accumulates into dlt[it % 3]; before arriving, CTA 0
+    // clears dlt[(it + 1) % 3] — last read in the finish of pass it − 2, which every CTA completed
+    // before it arrived at barrier it − 1 — so no CTA ever waits for the others to finish reading.
+    unsigned long long* dlt = a.dlt + (size_t)(it % 3) * nacc;
     for (int i = tid; i < nacc; i += kThreadsTC) {
       const unsigned long long v = s_acc[i];
-      if (v) atomicAdd(tot + i, v);
+      if (v) atomicAdd(dlt + i, v);
       s_acc[i] = 0ull;
+    }
+    if (blockIdx.x == 0) {
+      unsigned long long* nxt = a.dlt + (size_t)((it + 1) % 3) * nacc;
+      for (int i = tid; i < nacc; i += kThreadsTC) nxt[i] = 0ull;
     }
     __threadfence();
     __syncthreads();
@@ -967,6 +987,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
     }
     __syncthreads();
+    // running totals of the current labels, per CTA: S_t = S_{t−1} + Δ_t (exact int64)
+    for (int i = tid; i < nacc; i += kThreadsTC) {
+      const unsigned long long v = s_tot[i] + __ldcg(dlt + i);
+      s_tot[i] = v;
+      if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
+    }
+    __syncthreads();
+    const unsigned long long* tot = s_tot;
     // ---- resident finish (every CTA; CTA 0 publishes) — engine._finish_update / converged ----
     const bool pub = blockIdx.x == 0;
     bool stop = false;
@@ -974,7 +1002,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (exhausted) {
       // the final assign pass of an exhausted run: counts = bincount(L_T), C_T unchanged
       if (pub) {
-        for (int cc = tid; cc < k; cc += kThreadsTC) a.fin.model_counts[cc] = (long long)__ldcg(tot + km + cc);
+        for (int cc = tid; cc < k; cc += kThreadsTC) a.fin.model_counts[cc] = (long long)tot[km + cc];
         if (tid == 0) st->done = 1;
       }
       stop = true;
@@ -988,9 +1016,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       float wmax = 0.f;
       int wflags = 0;
       for (int c = warp; c < k; c += kThreadsTC / 32) {
-        const long long nc = (long long)__ldcg(tot + km + c);
+        const long long nc = (long long)tot[km + c];
         const bool fv = lane < m;
-        const long long sv = fv ? (long long)__ldcg(tot + (size_t)c * m + lane) : 0ll;
+        const long long sv = fv ? (long long)tot[(size_t)c * m + lane] : 0ll;
         // empty clusters get a placeholder; every one is re-seeded by the host repair
         const double v = (fv && nc > 0) ? __ddiv_rn(__dmul_rn((double)sv, a.fin.inv_scale), (double)nc) : 0.0;
         const double vo = fv ? C[(size_t)c * m + lane] : 0.0;
@@ -1044,10 +1072,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       }
       __syncthreads();
       if (pst && it < 256) atomicMax(pst + it * 8 + 5, globaltimer());
-      if (tid == 0) {  // this CTA is done reading the totals
-        __threadfence();
-        atomicAdd(a.grid_sync + 1, 1u);
-      }
       int flags = 0;
       float cmx = 0.f;
       for (int w = 0; w < kThreadsTC / 32; ++w) {
@@ -1059,7 +1083,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       if (flags & 1) {
         if (pub && tid == 0) {
           int ne = 0;
-          for (int c = 0; c < k; ++c) ne += (__ldcg(tot + km + c) == 0ull);
+          for (int c = 0; c < k; ++c) ne += (tot[km + c] == 0ull);
           st->n_empty = ne;
           st->need_host = 1;
         }

@@ -39,7 +39,8 @@ struct TcArgs {
   unsigned int* cta_done;  // completion counter for the fused finish (self-resetting)
   FinishArgs fin;
   int32_t resident;        // 1: run the whole loop in this (cooperative) launch, see lloyd_pass_tc_kernel
-  unsigned int* grid_sync; // resident: [0] barrier arrivals, [1] totals consumed (zeroed before the launch)
+  unsigned int* grid_sync; // resident: [0] barrier arrivals (zeroed before the launch)
+  unsigned long long* dlt; // resident: [3][k·m + k] per-pass deltas (zeroed before the launch)
   DevState* st;
   int32_t gate;
   float* dbg_scores;       // optional n × k raw tensor-core scores, unscaled (tests)
