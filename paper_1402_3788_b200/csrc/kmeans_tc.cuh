@@ -772,9 +772,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
       const int i0 = (e - (g0 & 1)) & 1;
-      int old_next[MB];
+      // previous labels prefetched two tiles of this group ahead (an L2 or DRAM round trip
+      // must not stall the epilogue)
+      int old_n1[MB], old_n2[MB];
 #pragma unroll
-      for (int mb = 0; mb < MB; ++mb) old_next[mb] = prev_label(i0, mb);
+      for (int mb = 0; mb < MB; ++mb) {
+        old_n1[mb] = prev_label(i0, mb);
+        old_n2[mb] = prev_label(i0 + kEpiGroups, mb);
+      }
       for (int i = i0; i < my_tiles && !(KM_DBG_FLAGS & 4); i += kEpiGroups) {
         const int g = g0 + i;
         const int ss = g % TM::NS;
@@ -784,8 +789,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         int olds[MB];
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
-          olds[mb] = old_next[mb];
-          old_next[mb] = prev_label(i + kEpiGroups, mb);  // prefetch one tile ahead (latency off the critical path)
+          olds[mb] = old_n1[mb];
+          old_n1[mb] = old_n2[mb];
+          old_n2[mb] = prev_label(i + 2 * kEpiGroups, mb);
         }
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
