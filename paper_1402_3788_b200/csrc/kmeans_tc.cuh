@@ -154,6 +154,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #if KM_WAIT_MODE == 1
   while (!mbar_test(bar, parity)) {
   }
+#elif KM_WAIT_MODE >= 3  // tuning: poll + fixed sleep (no wake-ups on unrelated barrier events)
+  uint32_t n = 0;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(KM_WAIT_MODE);
+    if (++n == (1u << 26)) __trap();
+  }
 #else
   uint32_t n = 0;
   while (!mbar_try(bar, parity)) {
