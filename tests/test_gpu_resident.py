@@ -1,0 +1,86 @@
+"""The resident Lloyd loop (one cooperative launch for the whole iteration,
+grid barrier between passes, per-CTA finish) against the launch-per-iteration
+kernel and the C oracle.
+
+Both paths must give bit-identical centres, counts, labels and iteration
+counts: the totals are exact int64 fixed-point sums and every CTA derives the
+same decisions from them.  KM_NO_RESIDENT=1 (read by km_lloyd at call time)
+forces the launch-per-iteration path.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def fit(x, c0, iters, tol=0.0, resident=True):
+    from paper_1402_3788_b200 import _native
+
+    if resident:
+        os.environ.pop("KM_NO_RESIDENT", None)
+    else:
+        os.environ["KM_NO_RESIDENT"] = "1"
+    try:
+        eng = _native.NativeEngine(0)
+        eng.load(x)
+        centers, counts, labels, it, conv = eng.lloyd(c0, iters, tol)
+        st = eng.stats()
+        eng.close()
+    finally:
+        os.environ.pop("KM_NO_RESIDENT", None)
+    return centers, counts, labels, it, conv, st
+
+
+@pytest.mark.parametrize("n,m,k,iters,tol", [(300_000, 25, 16, 60, 0.0), (100_000, 10, 8, 1000, 0.0),
+                                             (150_000, 5, 4, 1000, 1e-3), (80_000, 25, 64, 25, 0.0),
+                                             (60_000, 13, 40, 30, 0.0), (7_777, 25, 16, 1000, 0.0)])
+def test_resident_equals_per_iteration_launches(n, m, k, iters, tol):
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(n, m, k, seed=11 + n % 97, dtype=np.float32)
+    c0 = x[:k].astype(np.float64)
+    a = fit(x, c0, iters, tol, resident=True)
+    b = fit(x, c0, iters, tol, resident=False)
+    assert a[3] == b[3] and a[4] == b[4]
+    assert np.array_equal(a[0], b[0]), "centres must be bit-identical"
+    assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
+    # the resident run used few launches: one per empty-cluster repair round (+ the prep kernel)
+    assert a[5]["host_syncs"] <= b[5]["host_syncs"]
+
+
+def test_resident_repair_and_relaunch_vs_oracle():
+    """Duplicated initial centres: the duplicates come out empty after the first update, the
+    resident launch stops for the host repair, then a new launch continues the same loop."""
+    from oracle import oracle
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(120_000, 25, 16, seed=5, dtype=np.float32)
+    c0 = x[:16].astype(np.float64)
+    c0[5] = c0[3]
+    c0[9] = c0[3]
+    want = oracle.lloyd(x.astype(np.float64), c0, max_iters=200, n_workers=8)
+    centers, counts, labels, it, conv, st = fit(x, c0, 200)
+    assert st["repairs"] >= 1
+    assert it == want["iterations"] and conv == want["converged"]
+    assert np.array_equal(labels, want["labels"]) and np.array_equal(counts, want["counts"])
+    rel = np.max(np.abs(centers - want["centers"]) / np.maximum(np.abs(want["centers"]), 1.0))
+    assert rel <= 1e-12
+
+
+def test_resident_exhausted_counts_are_final_assignment():
+    """max_iters reached without convergence: one more assign pass inside the launch, counts =
+    bincount(L_T), labels = A(C_T) (engine.iterate's exhaustion rule)."""
+    from oracle import oracle
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(200_000, 25, 16, seed=2, dtype=np.float32)
+    c0 = x[:16].astype(np.float64)
+    for iters in (1, 2, 7):
+        want = oracle.lloyd(x.astype(np.float64), c0, max_iters=iters, n_workers=8)
+        centers, counts, labels, it, conv, _ = fit(x, c0, iters)
+        assert it == iters and not conv and not want["converged"]
+        assert np.array_equal(labels, want["labels"]) and np.array_equal(counts, want["counts"])
+        assert np.array_equal(np.bincount(labels, minlength=16), counts)
