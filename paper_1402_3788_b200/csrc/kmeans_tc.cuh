@@ -46,9 +46,15 @@ namespace tc {
 constexpr int kQueueCap = 768;                     // per-CTA staging of uncertified points (smem)
 constexpr long long kQueueFlag = 1ll << 62;
 constexpr int kTileRows = 128;
-constexpr int kTransformGroups = 2;                // transform warpgroups (alternate tiles)
+#ifndef KM_TRANSFORM_GROUPS
+#define KM_TRANSFORM_GROUPS 2
+#endif
+constexpr int kTransformGroups = KM_TRANSFORM_GROUPS;  // transform warpgroups (tile g → group g mod groups)
 constexpr int kTransformWarps = 4 * kTransformGroups;
-constexpr int kEpiGroups = 2;                      // epilogue warpgroups (alternate tiles)
+#ifndef KM_EPI_GROUPS
+#define KM_EPI_GROUPS 2
+#endif
+constexpr int kEpiGroups = KM_EPI_GROUPS;          // epilogue warpgroups (tile g → group g mod kEpiGroups)
 constexpr int kEpiWarps = 4 * kEpiGroups;
 constexpr int kProducerWarp = kTransformWarps + kEpiWarps;  // TMA producer
 constexpr int kMmaWarp = kProducerWarp + 1;                 // TMEM allocator + MMA issuer (even tiles)
@@ -61,7 +67,7 @@ constexpr int kThreadsTC = (kRecheckWarp + 1) * 32;
 // point where they fit; the A ring (transform → MMA) then holds one tile per transform group.
 template <int MP, int KP, int TR>
 struct TcBudget {
-  static constexpr int a = 4;  // two A buffers per transform group
+  static constexpr int a = 2 * kTransformGroups;  // two A buffers per transform group (a group owns buffers g mod a)
   static constexpr int mw = (KP + 31) / 32;
   static constexpr int raw_stride_max = ((TR * MP * 4 + 256 + 1023) / 1024) * 1024;
   static constexpr int fixed = a * TR * 128 + 2 * KP * 128 +                          // A ring, B tile
@@ -90,7 +96,7 @@ struct TcStages {
                                             TcBudget<MP, KP, 256>::raw_stride_max
                                       : TcBudget<MP, KP, 128>::raw;
   static constexpr int raw = raw_fit > 12 ? 12 : raw_fit;
-  static constexpr int a = 4;
+  static constexpr int a = 2 * kTransformGroups;
   static_assert(raw >= 2, "shared-memory budget");
 };
 
@@ -460,7 +466,7 @@ __device__ __forceinline__ int exact_candidates(const float* __restrict__ gx, in
 //   clusters (the host repairs them and relaunches).
 template <int MT, int KP, bool PRE>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
-  static_assert(kThreadsTC == 640, "warp-role layout");
+  static_assert(kThreadsTC == (kTransformWarps + kEpiWarps + 4) * 32, "warp-role layout");
   constexpr int MP = MT > 0 ? MT : -MT;
   if (a.gate && (a.st->done || a.st->need_host)) return;
   using L = TcLayout<MP>;
@@ -682,7 +688,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
       const int key = p & 7;
       const float* __restrict__ gx = a.x;
-      for (int i = (tg - (g0 & 1)) & 1; i < my_tiles; i += kTransformGroups) {
+      for (int i = ((tg - g0) % kTransformGroups + kTransformGroups) % kTransformGroups; i < my_tiles;
+           i += kTransformGroups) {
         const int g = g0 + i;
         const int s = g % RS, sa = g % AS;
         const int64_t row0 = (t_lo + i) * TR;
@@ -777,7 +784,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const int64_t r = (t_lo + i) * TR + 128 * mb + p;
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
-      const int i0 = (e - (g0 & 1)) & 1;
+      const int i0 = ((e - g0) % kEpiGroups + kEpiGroups) % kEpiGroups;
       // previous labels prefetched two tiles of this group ahead (an L2 or DRAM round trip
       // must not stall the epilogue)
       int old_n1[MB], old_n2[MB];
