@@ -123,6 +123,19 @@ KM_API int km_wcss(km_engine* e, const double* centers, int32_t k, const int64_t
  * out (n×k fp64) = Euclidean distance of every resident point to every centre. */
 KM_API int km_center_distances(km_engine* e, const double* centers, int32_t k, double* out);
 
+/* ---- seeding ----
+ * km_diameter: largest pairwise distance over rows scan_rows(n, pair_cap) × all j > i
+ *   (engine.diameter / _kernels.max_pair_rows, engine.py:124-154, _kernels.py:49-81): exact
+ *   fp64 value of the reference recurrence, ties → smallest (i, j).  pair_cap <= 0: every pair.
+ * km_seed_reset / km_seed_add / km_seed_min_d2: the per-sample minimum squared distance to the
+ *   chosen centres (engine._append_center / _kernels.update_min_d2, engine.py:157-160,
+ *   _kernels.py:144-155, fp64, same recurrence); km_seed_add lowers it with sample c and returns
+ *   np.argmax of the result (largest, lowest index) — the maximin step (engine.py:162-168). */
+KM_API int km_diameter(km_engine* e, int64_t pair_cap, double* d_out, int64_t* i_out, int64_t* j_out);
+KM_API int km_seed_reset(km_engine* e);
+KM_API int km_seed_add(km_engine* e, int64_t c, double* max_v, int64_t* max_i);
+KM_API int km_seed_min_d2(km_engine* e, int64_t i, double* out);
+
 /* ---- row-sharded multi-GPU step API (partition.py:84-100,237-261) ------
  * One process per GPU holds a contiguous row shard.  Per iteration:
  *   km_step_pass      fused assign + per-cluster fixed-point sums of the shard

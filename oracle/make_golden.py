@@ -194,5 +194,60 @@ def main():
     print("done")
 
 
+def seeding():
+    """Seeding phase + full run_single (engine.py:124-215, 346-370): diameter (optionally with a
+    pair cap), maximin / random-far initial centres, the Lloyd result and its wcss, plus
+    degenerate cases (fewer distinct points than k)."""
+    from kmeans_regimes.engine import global_centroid_of, run_single  # noqa: E402
+    from kmeans_regimes.exceptions import DegenerateDataError  # noqa: E402
+
+    _kernels.warmup()
+    rng = np.random.default_rng(424242)
+    cases = {}
+    specs = []
+    for t in range(24):
+        n = int(rng.integers(2, 600))
+        m = int(rng.integers(1, 10))
+        kind = int(rng.integers(0, 3))
+        coords = random_coords(rng, n, m, kind=kind)
+        if t % 2:
+            coords = coords.astype(np.float32).astype(np.float64)
+        k = int(rng.integers(1, min(9, n) + 1))
+        init = "maximin" if t % 3 else "random-far"
+        cap = None if t % 4 else int(rng.integers(1, max(2, n * (n - 1) // 2)))
+        specs.append((coords, k, init, int(t), cap))
+    for name, (n, m, k, seed) in {"s_synth_3k_5_4": (3000, 5, 4, 2), "s_synth_5k_25_16": (5000, 25, 16, 4)}.items():
+        coords = generate_synthetic(n, m, k, seed=seed).coords.astype(np.float32).astype(np.float64)
+        specs.append((coords, k, "maximin", seed, None))
+        specs.append((coords, k, "random-far", seed, 20_000))
+    dup = np.repeat(np.array([[1.0, 2.0], [3.0, 4.0]]), 5, axis=0)
+    specs.append((dup, 3, "maximin", 0, None))          # 2 distinct points, k = 3 → degenerate
+    specs.append((np.zeros((4, 3)), 2, "maximin", 0, None))  # diameter 0 → degenerate at the 2nd centre
+    for t, (coords, k, init, seed, cap) in enumerate(specs):
+        ds = Dataset(coords)
+        cfg = KmeansConfig(k=k, init=init, seed=seed, diameter_pair_cap=cap)
+        diam = diameter(ds, pair_cap=cap)
+        rec = dict(coords=coords, k=np.int64(k), init=np.bytes_(init), seed=np.int64(seed),
+                   cap=np.int64(-1 if cap is None else cap), d=np.float64(diam.d), i=np.int64(diam.i),
+                   j=np.int64(diam.j), centroid=global_centroid_of(ds))
+        try:
+            c0 = init_centers(ds, cfg, diam).centers
+            res = run_single(ds, cfg)
+            rec.update(degenerate=np.bool_(False), c0=c0, labels=res.assignment.labels,
+                       centers=res.model.centers, counts=res.model.counts, iterations=np.int64(res.iterations),
+                       converged=np.bool_(res.converged),
+                       inertia=np.float64(wcss(ds, res.model, res.assignment)))
+        except DegenerateDataError:
+            rec.update(degenerate=np.bool_(True))
+        cases[t] = rec
+    np.savez_compressed(OUT / "seeding.npz", **{f"{key}_{t}": v for t, d in cases.items() for key, v in d.items()},
+                        count=np.int64(len(cases)))
+    print(f"seeding: {len(cases)} cases ({sum(bool(d['degenerate']) for d in cases.values())} degenerate)")
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["seeding"]:
+        seeding()
+    else:
+        main()
+        seeding()

@@ -140,3 +140,100 @@ def lloyd(coords, c0, max_iters=1000, tol=0.0, block=DEFAULT_BLOCK, n_workers=1)
 
 def cpu_count():
     return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# Seeding, restated in numpy: elementwise fp64 operations in the
+# reference's feature order (numpy never fuses a multiply-add), so every squared
+# distance is bit-identical to the numba kernels.
+# ---------------------------------------------------------------------------
+class DegenerateData(Exception):
+    """engine.py:162-168 / :190-193 (DegenerateDataError)."""
+
+
+def scan_rows(n, pair_cap=None):
+    """engine.scan_rows (engine.py:124-138)."""
+    import math
+
+    if n < 2:
+        return np.empty(0, dtype=np.int64)
+    total = n * (n - 1) // 2
+    if pair_cap is None or total <= pair_cap:
+        return np.arange(n - 1, dtype=np.int64)
+    stride = max(2, math.ceil(total / pair_cap))
+    return np.arange(0, n - 1, stride, dtype=np.int64)
+
+
+def diameter(coords, pair_cap=None):
+    """engine.diameter + _kernels.max_pair_rows (engine.py:141-154, _kernels.py:49-81):
+    rows ascending, j > i ascending, d² = Σ_f (x_if − x_jf)² left to right, strict '>'
+    (the first maximum in scan order = smallest (i, j)).  Returns (d, i, j)."""
+    x = _f64(coords)
+    n, m = x.shape
+    best, bi, bj = -1.0, -1, -1
+    for i in scan_rows(n, pair_cap):
+        rest = x[i + 1:]
+        d2 = np.zeros(rest.shape[0])
+        for f in range(m):
+            d = x[i, f] - rest[:, f]
+            d2 += d * d
+        if d2.size:
+            jj = int(np.argmax(d2))
+            if d2[jj] > best:
+                best, bi, bj = float(d2[jj]), int(i), int(i + 1 + jj)
+    return float(np.sqrt(best)), bi, bj
+
+
+def _lower_min_d2(x, c, min_d2):
+    """_kernels.update_min_d2 (_kernels.py:144-155)."""
+    d2 = np.zeros(x.shape[0])
+    for f in range(x.shape[1]):
+        d = x[:, f] - x[c, f]
+        d2 += d * d
+    np.minimum(min_d2, d2, out=min_d2)
+
+
+def init_centers(coords, k, init="maximin", seed=0, diam=None):
+    """engine.init_centers (engine.py:171-215) → (k, m) initial centres."""
+    x = _f64(coords)
+    n = x.shape[0]
+    if diam is None:
+        diam = diameter(x)
+    d, i0, j0 = diam
+    min_d2 = np.full(n, np.inf)
+    chosen = []
+
+    def append(idx):
+        chosen.append(int(idx))
+        _lower_min_d2(x, int(idx), min_d2)
+
+    def farthest():
+        idx = int(np.argmax(min_d2))
+        if min_d2[idx] == 0.0:
+            raise DegenerateData("dataset has fewer distinct points than requested centers")
+        return idx
+
+    if init == "maximin":
+        append(i0)
+        if k >= 2:
+            if d == 0.0:
+                raise DegenerateData("dataset has fewer distinct points than requested centers")
+            append(j0)
+        while len(chosen) < k:
+            append(farthest())
+    else:
+        rng = np.random.default_rng(seed)
+        thr2 = (d / (2.0 * k)) ** 2
+        draws, limit = 0, 10 * n
+        while len(chosen) < k:
+            accepted = False
+            while draws < limit:
+                cand = int(rng.integers(n))
+                draws += 1
+                if not chosen or min_d2[cand] > thr2:
+                    append(cand)
+                    accepted = True
+                    break
+            if not accepted:
+                append(farthest())
+    return x[np.asarray(chosen, dtype=np.int64)].copy()

@@ -15,11 +15,15 @@ from .engine import (
     KmeansResult,
     assign_step,
     converged,
+    diameter,
     global_centroid_of,
+    init_centers,
     iterate,
     run_b200,
+    scan_rows,
     update_step,
 )
+from .estimator import RegimeKMeans
 from .exceptions import (
     CapacityExceededError,
     ClusteringError,
@@ -55,6 +59,7 @@ from .model import (
 __version__ = "0.1.0"
 
 __all__ = [
+    "RegimeKMeans", "diameter", "init_centers", "scan_rows",
     "Assignment", "CapacityExceededError", "ClusterModel", "ClusteringError", "ContractViolationError",
     "DataFormatError", "Dataset", "DEFAULT_BLOCK", "DegenerateDataError", "DeviceLostError",
     "DeviceUnavailableError", "DiameterResult", "DoubleCollectError", "EmptyClusterError",

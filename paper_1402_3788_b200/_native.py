@@ -70,6 +70,10 @@ SIGNATURES = {
     "km_lloyd": (ctypes.c_int, [P, P, I32, I32, F64, P, P, P, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
     "km_wcss": (ctypes.c_int, [P, P, I32, P, ctypes.POINTER(F64)]),
     "km_center_distances": (ctypes.c_int, [P, P, I32, P]),
+    "km_diameter": (ctypes.c_int, [P, I64, ctypes.POINTER(F64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+    "km_seed_reset": (ctypes.c_int, [P]),
+    "km_seed_add": (ctypes.c_int, [P, I64, ctypes.POINTER(F64), ctypes.POINTER(I64)]),
+    "km_seed_min_d2": (ctypes.c_int, [P, I64, ctypes.POINTER(F64)]),
     "km_set_frac_bits": (ctypes.c_int, [P, I32]),
     "km_frac_bits_for": (ctypes.c_int, [F64, I64, ctypes.POINTER(I32)]),
     "km_step_begin": (ctypes.c_int, [P, P, I32]),
@@ -232,6 +236,28 @@ class NativeEngine:
         out = np.empty((self.n, centers.shape[0]), dtype=np.float64)
         self._check(self._lib.km_center_distances(self._h, _ptr(centers), centers.shape[0], _ptr(out)))
         return out
+
+    # -- seeding -------------------------------------------------
+    def diameter(self, pair_cap=None):
+        """(d, i, j): largest pairwise distance over engine.scan_rows(n, pair_cap) rows."""
+        d, i, j = F64(), I64(), I64()
+        cap = 0 if pair_cap is None else int(pair_cap)
+        self._check(self._lib.km_diameter(self._h, cap, ctypes.byref(d), ctypes.byref(i), ctypes.byref(j)))
+        return d.value, i.value, j.value
+
+    def seed_reset(self):
+        self._check(self._lib.km_seed_reset(self._h))
+
+    def seed_add(self, c: int):
+        """Lower min_d2 with sample c; returns (max min_d2, its first index)."""
+        v, i = F64(), I64()
+        self._check(self._lib.km_seed_add(self._h, int(c), ctypes.byref(v), ctypes.byref(i)))
+        return v.value, i.value
+
+    def seed_min_d2(self, i: int) -> float:
+        v = F64()
+        self._check(self._lib.km_seed_min_d2(self._h, int(i), ctypes.byref(v)))
+        return v.value
 
     # -- step API (multi-GPU) -------------------------------------------------
     def set_frac_bits(self, f: int):

@@ -18,6 +18,7 @@
 
 #include "../../include/kmeans_b200.h"
 #include "kmeans_kernels.cuh"
+#include "kmeans_seed.cuh"
 #include "kmeans_tc.h"
 
 using namespace km;
@@ -39,6 +40,12 @@ struct km_engine {
   void* xbuf = nullptr;             // owned points (fp32, or fp64 when narrowing would lose bits)
   void* stage = nullptr;            // fp64 upload staging
   size_t xbuf_cap = 0, stage_cap = 0, labels_cap = 0, rr_cap = 0, d2_cap = 0, l64_cap = 0, partials_cap = 0;
+  // seeding: per-block pair-scan bests, min_d2 argmax partials
+  PairBest* pair_best = nullptr;
+  double* seed_pv = nullptr;
+  long long* seed_pi = nullptr;
+  size_t pair_best_cap = 0, seed_pv_cap = 0, seed_pi_cap = 0;
+  bool seed_ready = false;
   int64_t n = 0;
   int32_t m = 0;
   int32_t point_bytes = 4;
@@ -623,6 +630,7 @@ static int after_points_loaded(km_engine* e) {
 
 static int drop_points(km_engine* e) {
   free_k(e);
+  e->seed_ready = false;
   e->x = nullptr;  // an owned copy lives on in xbuf / stage for the next load
   e->x_owned = false;
   e->n = 0;
@@ -763,6 +771,7 @@ int km_destroy(km_engine* e) {
   drop_points(e);
   dfree(e->xbuf); dfree(e->stage); dfree(e->labels); dfree(e->recheck_rows); dfree(e->d2);
   dfree(e->labels64); dfree(e->partials);
+  dfree(e->pair_best); dfree(e->seed_pv); dfree(e->seed_pi);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   dfree(e->st);
   dfree(e->scratch_u);
@@ -1156,6 +1165,131 @@ int km_wcss(km_engine* e, const double* centers, int32_t k, const int64_t* label
   CK(cudaMemcpyAsync(&v, e->scratch_u, 8, cudaMemcpyDeviceToHost, e->stream));
   CK(cudaStreamSynchronize(e->stream));
   *out = std::ldexp((double)(long long)v, -F2);
+  return KM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Seeding: diameter pair scan + maximin / random-far primitives
+// ---------------------------------------------------------------------------
+int km_diameter(km_engine* e, int64_t pair_cap, double* d_out, int64_t* i_out, int64_t* j_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  cudaSetDevice(e->device);
+  const int64_t n = e->n;
+  const int m = e->m;
+  if (n < 2) return set_err(e, KM_ERR_CONTRACT, "diameter needs at least 2 samples, got %lld", (long long)n);
+  // engine.scan_rows (engine.py:124-138): every row, or every stride-th row under a pair cap
+  const unsigned __int128 total = (unsigned __int128)n * (unsigned __int128)(n - 1) / 2;
+  int64_t stride = 1;
+  if (pair_cap > 0 && total > (unsigned __int128)pair_cap) {
+    const unsigned __int128 q = (total + (unsigned __int128)pair_cap - 1) / (unsigned __int128)pair_cap;
+    stride = std::max<int64_t>(2, (int64_t)q);
+  }
+  const int64_t R = (n - 1 + stride - 1) / stride;
+  const int grid = e->num_sms * 4;
+  int r;
+  if ((r = grow(e, &e->pair_best, &e->pair_best_cap, sizeof(PairBest) * (size_t)grid))) return r;
+  // fp32 estimates are certified only for fp32-exact points whose squares stay normal
+  bool exact = e->point_bytes != 4 || !(e->absmax < std::ldexp(1.0, 60));
+  float thr = -1.0f;
+  if (!exact) {
+    unsigned int zero = 0, bits = 0;
+    CK(cudaMemcpyAsync(e->scratch_u, &zero, 4, cudaMemcpyHostToDevice, e->stream));
+    pair_scan_kernel<float, false><<<grid, kPairCols, 0, e->stream>>>((const float*)e->x, n, m, stride, R, 0.f,
+                                                                      (unsigned int*)e->scratch_u, e->pair_best);
+    CK_LAUNCH("pair_scan_kernel (phase 1)");
+    e->stats.kernel_launches += 1;
+    CK(cudaMemcpyAsync(&bits, e->scratch_u, 4, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    float max32;
+    std::memcpy(&max32, &bits, 4);
+    if (!(max32 >= std::ldexp(1.0f, -100))) {
+      exact = true;
+    } else {
+      // relative error of a fp32 squared distance of fp32 points (+ the reference's fp64 rounding)
+      const double g = (m + 4) * std::ldexp(1.0, -24) * 1.01 + (m + 2) * std::ldexp(1.0, -52);
+      const double t = (double)max32 * (1.0 - g) / (1.0 + g) - m * std::ldexp(1.0, -120);
+      thr = std::nextafter((float)t, -INFINITY);
+    }
+  }
+  if (e->point_bytes == 4)
+    pair_scan_kernel<float, true><<<grid, kPairCols, 0, e->stream>>>((const float*)e->x, n, m, stride, R,
+                                                                     exact ? -1.0f : thr, nullptr, e->pair_best);
+  else
+    pair_scan_kernel<double, true><<<grid, kPairCols, 0, e->stream>>>((const double*)e->x, n, m, stride, R, -1.0f,
+                                                                      nullptr, e->pair_best);
+  CK_LAUNCH("pair_scan_kernel (phase 2)");
+  e->stats.kernel_launches += 1;
+  std::vector<PairBest> h(grid);
+  CK(cudaMemcpyAsync(h.data(), e->pair_best, sizeof(PairBest) * grid, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  PairBest best{-1.0, -1, -1};
+  for (const PairBest& b : h) {
+    if (b.i < 0) continue;
+    if (best.i < 0 || b.d2 > best.d2 || (b.d2 == best.d2 && (b.i < best.i || (b.i == best.i && b.j < best.j))))
+      best = b;
+  }
+  if (d_out) *d_out = std::sqrt(best.d2);
+  if (i_out) *i_out = best.i;
+  if (j_out) *j_out = best.j;
+  return KM_OK;
+}
+
+static int seed_argmax(km_engine* e, int grid, double* v_out, int64_t* i_out) {
+  std::vector<double> pv(grid);
+  std::vector<long long> pi(grid);
+  CK(cudaMemcpyAsync(pv.data(), e->seed_pv, 8 * (size_t)grid, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaMemcpyAsync(pi.data(), e->seed_pi, 8 * (size_t)grid, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  double bv = -1.0;
+  long long bi = -1;
+  for (int b = 0; b < grid; ++b)
+    if (pi[b] < e->n && (bi < 0 || pv[b] > bv || (pv[b] == bv && pi[b] < bi))) { bv = pv[b]; bi = pi[b]; }
+  if (v_out) *v_out = bv;
+  if (i_out) *i_out = bi;
+  return KM_OK;
+}
+
+int km_seed_reset(km_engine* e) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  cudaSetDevice(e->device);
+  int r;
+  if ((r = grow(e, &e->d2, &e->d2_cap, 8 * (size_t)e->n))) return r;
+  fill_f64_kernel<<<grid_for(e, e->n, 4), 256, 0, e->stream>>>(e->d2, e->n, INFINITY);
+  CK_LAUNCH("fill_f64_kernel");
+  e->stats.kernel_launches += 1;
+  e->seed_ready = true;
+  return KM_OK;
+}
+
+int km_seed_add(km_engine* e, int64_t c, double* max_v, int64_t* max_i) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x || !e->seed_ready) return set_err(e, KM_ERR_CONTRACT, "call km_seed_reset first");
+  if (c < 0 || c >= e->n) return set_err(e, KM_ERR_CONTRACT, "centre index %lld out of range", (long long)c);
+  cudaSetDevice(e->device);
+  const int grid = grid_for(e, e->n, 4);
+  int r;
+  if ((r = grow(e, &e->seed_pv, &e->seed_pv_cap, 8 * (size_t)grid))) return r;
+  if ((r = grow(e, &e->seed_pi, &e->seed_pi_cap, 8 * (size_t)grid))) return r;
+  const size_t smem = 8 * (size_t)e->m;
+  if (e->point_bytes == 4)
+    min_d2_update_kernel<float><<<grid, 256, smem, e->stream>>>((const float*)e->x, e->n, e->m, c, e->d2, e->seed_pv,
+                                                                 e->seed_pi);
+  else
+    min_d2_update_kernel<double><<<grid, 256, smem, e->stream>>>((const double*)e->x, e->n, e->m, c, e->d2,
+                                                                  e->seed_pv, e->seed_pi);
+  CK_LAUNCH("min_d2_update_kernel");
+  e->stats.kernel_launches += 1;
+  return seed_argmax(e, grid, max_v, max_i);
+}
+
+int km_seed_min_d2(km_engine* e, int64_t i, double* out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x || !e->seed_ready) return set_err(e, KM_ERR_CONTRACT, "call km_seed_reset first");
+  if (i < 0 || i >= e->n) return set_err(e, KM_ERR_CONTRACT, "sample index %lld out of range", (long long)i);
+  CK(cudaMemcpyAsync(out, e->d2 + i, 8, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
   return KM_OK;
 }
 

@@ -18,7 +18,9 @@ from typing import Optional
 
 import numpy as np
 
-from .exceptions import ContractViolationError
+import math
+
+from .exceptions import ContractViolationError, DegenerateDataError, InsufficientDataError
 from .model import DEFAULT_BLOCK, SUPPORTED_METRICS, Assignment, ClusterModel, Dataset, wcss
 from .validation import check_coordinates, check_labels
 
@@ -166,6 +168,78 @@ def global_centroid_of(dataset, *, block=DEFAULT_BLOCK):
     return centroid_of(_dataset(dataset), block=block)
 
 
+def scan_rows(n, pair_cap=None):
+    """Row indices the diameter scan visits (engine.py:124-138), as a pure function of (n, cap)."""
+    if n < 2:
+        return np.empty(0, dtype=np.int64)
+    total = n * (n - 1) // 2
+    if pair_cap is None or total <= pair_cap:
+        return np.arange(n - 1, dtype=np.int64)
+    stride = max(2, math.ceil(total / pair_cap))
+    return np.arange(0, n - 1, stride, dtype=np.int64)
+
+
+def diameter(dataset, *, pair_cap=None, device=0):
+    """Largest pairwise distance (engine.py:141-154) on the device: exact fp64 value of the
+    reference recurrence, ties → smallest (i, j), rows per ``scan_rows``."""
+    dataset = _dataset(dataset)
+    if dataset.n < 2:
+        raise InsufficientDataError(f"diameter needs at least 2 samples, got {dataset.n}")
+    d, i, j = dataset.device_engine(device).diameter(pair_cap)
+    return DiameterResult(float(d), int(i), int(j))
+
+
+def init_centers(dataset, config, diam, global_centroid=None, *, device=0):
+    """The k initial centres (engine.py:171-215): maximin (diameter pair, then the sample
+    farthest from the chosen ones, lowest index on ties) or random-far (seeded uniform draws
+    kept when farther than D/(2k), maximin fallback after 10n rejected draws).  The per-sample
+    minimum distances live on the device (exact fp64 recurrence); only the draw logic runs here.
+    """
+    dataset = _dataset(dataset)
+    config.validate_for(dataset)
+    eng = dataset.device_engine(device)
+    n, k = dataset.n, config.k
+    eng.seed_reset()
+    chosen = []
+    far = [0.0, -1]  # (max min_d2, its first index) after the last addition
+
+    def append(index):
+        chosen.append(int(index))
+        far[0], far[1] = eng.seed_add(int(index))
+
+    def farthest_unchosen():
+        if far[0] == 0.0:
+            raise DegenerateDataError("dataset has fewer distinct points than requested centers")
+        return far[1]
+
+    if config.init == "maximin":
+        append(diam.i)
+        if k >= 2:
+            if diam.d == 0.0:
+                raise DegenerateDataError("dataset has fewer distinct points than requested centers")
+            append(diam.j)
+        while len(chosen) < k:
+            append(farthest_unchosen())
+    else:
+        rng = np.random.default_rng(config.seed)
+        thr2 = (diam.d / (2.0 * k)) ** 2
+        draws = 0
+        limit = 10 * n
+        while len(chosen) < k:
+            accepted = False
+            while draws < limit:
+                cand = int(rng.integers(n))
+                draws += 1
+                if not chosen or eng.seed_min_d2(cand) > thr2:
+                    append(cand)
+                    accepted = True
+                    break
+            if not accepted:
+                append(farthest_unchosen())
+    centers = dataset.coords[np.asarray(chosen, dtype=np.int64)].astype(np.float64)
+    return ClusterModel(centers, np.zeros(k, dtype=np.int64))
+
+
 def run_b200(dataset, config, *, init_centers=None, device=0, want_labels=True):
     """Cluster with the device-resident Lloyd loop.
 
@@ -177,9 +251,11 @@ def run_b200(dataset, config, *, init_centers=None, device=0, want_labels=True):
     """
     dataset = _dataset(dataset)
     config.validate_for(dataset)
-    if init_centers is None:
-        raise NotImplementedError(
-            "device seeding (diameter / maximin, SURVEY §8f #1) is not built yet: pass init_centers")
+    diam = centroid = None
+    if init_centers is None:  # the reference's seeding phase (run_single, engine.py:358-362), on the device
+        diam = diameter(dataset, pair_cap=config.diameter_pair_cap, device=device)
+        centroid = global_centroid_of(dataset, block=config.accum_block)
+        init_centers = globals()["init_centers"](dataset, config, diam, centroid, device=device).centers
     c0 = check_coordinates(init_centers, name="init_centers")
     if c0.shape != (config.k, dataset.m):
         raise ContractViolationError(f"init_centers must have shape ({config.k}, {dataset.m}), got {c0.shape}")
@@ -191,7 +267,7 @@ def run_b200(dataset, config, *, init_centers=None, device=0, want_labels=True):
             lambda mdl: assign_step(dataset, mdl),
             lambda a: update_step(dataset, a, config.k),
         )
-        return KmeansResult(model, assignment, iterations, done, None, None, history)
+        return KmeansResult(model, assignment, iterations, done, diam, centroid, history)
     centers, counts, labels, iters, conv = eng.lloyd(c0, config.max_iters, config.tol, want_labels=want_labels)
     return KmeansResult(ClusterModel(centers, counts), Assignment(labels if labels is not None else np.empty(0)),
-                        iters, conv, None, None, None)
+                        iters, conv, diam, centroid, None)
