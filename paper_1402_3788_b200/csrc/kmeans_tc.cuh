@@ -65,12 +65,20 @@ constexpr int kThreadsTC = (kRecheckWarp + 1) * 32;
 // shared memory the other sections leave (~64 KB in flight per SM covers the loaded DRAM
 // latency).  Tiles of 256 points (two M=128 MMA blocks) halve every per-tile handshake per
 // point where they fit; the A ring (transform → MMA) then holds one tile per transform group.
+#ifndef KM_A_IN_TMEM
+#define KM_A_IN_TMEM 1
+#endif
+// A operand in TMEM (transform → tcgen05.st, MMA reads it from TMEM) when its columns fit next
+// to the score ring; otherwise the A tile is staged in shared memory (SW128)
+template <int KP, int TR>
+__host__ __device__ constexpr bool tc_a_in_tmem() { return KM_A_IN_TMEM && KP <= 32 && TR == 128; }
+
 template <int MP, int KP, int TR>
 struct TcBudget {
   static constexpr int a = 2 * kTransformGroups;  // two A buffers per transform group (a group owns buffers g mod a)
   static constexpr int mw = (KP + 31) / 32;
   static constexpr int raw_stride_max = ((TR * MP * 4 + 256 + 1023) / 1024) * 1024;
-  static constexpr int fixed = a * TR * 128 + 2 * KP * 128 +                          // A ring, B tile
+  static constexpr int fixed = (tc_a_in_tmem<KP, TR>() ? 0 : a * TR * 128) + 2 * KP * 128 +  // A ring, B tile
                                ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024 +       // Δ accumulators
                                kQueueCap * (8 + 4 * mw) + 1024 +                       // recheck queue
                                2048 + 1024 + 8192;                                     // barriers, align, static
@@ -250,6 +258,38 @@ __device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a_desc, uint64
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// A operand from TMEM ("TS"): a_tmem = column address of the 128-lane × K tile (2 halfs per column)
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, {%5, %6, %7, %8}, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+// 32 lanes × 8 / 16 / 32 columns of 32-bit from registers: thread i of the warp → lane (base + i)
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3])
+               : "memory");
+}
+// n (multiple of 4, compile-time) consecutive columns
+template <int N>
+__device__ __forceinline__ void tmem_st_row(uint32_t taddr, const uint32_t* r) {
+#pragma unroll
+  for (int c = 0; c + 8 <= N; c += 8) tmem_st8(taddr + c, r + c);
+  if constexpr (N % 8 == 4) tmem_st4(taddr + (N - 4), r + (N - 4));
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                        uint32_t accumulate) {
   asm volatile(
@@ -316,11 +356,14 @@ struct TcLayout {
   static constexpr int KSTEPS = (2 * HW) / 16;       // kind::f16 MMA k-steps (16 halfs = 32 B each)
 };
 
-template <int KP, int MB>
+template <int KP, int MB, int HW = 32, int AS = 0>
 struct TcTmem {
-  static constexpr int per = MB * 2 * KP;                                  // columns per tile
-  static constexpr int NS = 512 / per >= 8 ? 8 : 512 / per;                // TMEM score buffers
-  static constexpr uint32_t cols = NS * per;
+  static constexpr int per = MB * 2 * KP;                                  // score columns per tile
+  static constexpr int acols = AS * MB * HW;                               // TS: A buffers (HW columns per row block)
+  static constexpr int NS0 = (512 - acols) / per;
+  static constexpr int NS = NS0 >= 8 ? 8 : NS0;                            // TMEM score buffers
+  static constexpr uint32_t a_base = NS * per;                             // first A column (TS)
+  static constexpr uint32_t cols = NS * per + acols;
   static constexpr uint32_t alloc = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
 };
 
@@ -336,7 +379,7 @@ struct TcSmem {
     off_bar = 0;                              // mbarriers + TMEM address (1 KiB)
     off_w = 1024;                             // [2KP rows × 128 B] B operand (SW128)
     off_a = off_w + 2 * KP * 128;             // [AS][TR rows × 128 B]
-    off_acc = off_a + AS * TcStages<MP, KP>::TR * 128;                    // [KP·(MP+1) + KP] int64 Δ
+    off_acc = off_a + (tc_a_in_tmem<KP, TcStages<MP, KP>::TR>() ? 0 : AS * TcStages<MP, KP>::TR * 128);                    // [KP·(MP+1) + KP] int64 Δ
     off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;    // recheck queue: rows, masks, scalars
     off_raw = off_q + ((kQueueCap * (8 + 4 * ((KP + 31) / 32)) + 1024) + 1023) / 1024 * 1024;
     // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
@@ -472,7 +515,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   using L = TcLayout<MP>;
   constexpr int TR = TcStages<MP, KP>::TR;  // points per tile
   constexpr int MB = TR / 128;              // M=128 MMA blocks per tile
-  using TM = TcTmem<KP, MB>;
+  // A operand in TMEM (written by the transform with tcgen05.st, read by the MMA): takes the A
+  // tile off shared memory (its stores and the MMA's operand reads) where the columns fit
+  constexpr bool TS = tc_a_in_tmem<KP, TR>();
+  using TM = TcTmem<KP, MB, TcLayout<MP>::HW, TS ? TcStages<MP, KP>::a : 0>;
   const bool resident = a.resident != 0;
   const TcSmem<MP, KP> S(MT > 0 ? MT : a.m, resident ? a.k : 0);
   constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
@@ -535,7 +581,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       *reinterpret_cast<uint4*>(s_w + sw128(r, q)) = *reinterpret_cast<const uint4*>(a.wop + (size_t)r * 64 + q * 8);
     }
     // A operand buffers zeroed once (chunks beyond the used width stay zero)
-    for (int i = tid; i < AS * TR * 8; i += nthr)
+    if (!TS)
+      for (int i = tid; i < AS * TR * 8; i += nthr)
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
     for (int i = tid; i < kQueueCap; i += nthr) s_q[i] = 0;
@@ -669,11 +716,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         if (elect_one()) {
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb) {  // block mb: points 128·mb.. of the tile → columns mb·2KP..
-            const uint64_t adesc0 = make_desc(a0 + sa * (TR * 128) + mb * (128 * 128), 16, 1024);
             const uint32_t dcol = tm + ss * TM::per + mb * 2 * KP;
+            if constexpr (TS) {  // A from TMEM: 16 halfs = 8 columns per k-step
+              const uint32_t at = tm + TM::a_base + (uint32_t)(sa * L::HW);
 #pragma unroll
-            for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
-              mma_f16(dcol, adesc0 + 2 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+              for (int ks = 0; ks < L::KSTEPS; ++ks)
+                mma_f16_ts(dcol, at + 8 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+            } else {
+              const uint64_t adesc0 = make_desc(a0 + sa * (TR * 128) + mb * (128 * 128), 16, 1024);
+#pragma unroll
+              for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
+                mma_f16(dcol, adesc0 + 2 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+            }
           }
           mma_commit(s_full + ss);   // scores ready
           mma_commit(a_empty + sa);  // A buffer consumed
@@ -745,13 +799,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
             lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
           }
-          unsigned char* s_ab = s_a + mb * (128 * 128);
+          if constexpr (TS) {
+            // the point's A row [xh | xl] (HW 32-bit columns) → TMEM lane p of this tile's A buffer
+            const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + TM::a_base + (uint32_t)(sa * L::HW);
+            tmem_st_row<L::HW / 2>(ta, hw);
+            tmem_st_row<L::HW / 2>(ta + L::HW / 2, lw);
+          } else {
+            unsigned char* s_ab = s_a + mb * (128 * 128);
 #pragma unroll
-          for (int q = 0; q < L::HW / 8; ++q) {
-            *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)(q ^ key) << 4)) =
-                make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-            *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
-                make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+            for (int q = 0; q < L::HW / 8; ++q) {
+              *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)(q ^ key) << 4)) =
+                  make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+              *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
+                  make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+            }
           }
         }
         // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
@@ -759,7 +820,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         __syncwarp();
         if (lane == 0) mbar_arrive(empty_raw + s);
         if (stamp) ts[2] = clock64();
-        fence_proxy_async();
+        if constexpr (TS) {
+          tmem_st_wait();      // the A row is in TMEM
+          tc_fence_before();   // ordered before the hand-off to the MMA issuer
+        } else {
+          fence_proxy_async();  // generic-proxy A stores → visible to the tensor core
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full + sa);
         if (stamp) ts[3] = clock64();
