@@ -356,10 +356,15 @@ struct TcLayout {
   static constexpr int KSTEPS = (2 * HW) / 16;       // kind::f16 MMA k-steps (16 halfs = 32 B each)
 };
 
-template <int KP, int MB, int HW = 32, int AS = 0>
+// K3: the MMA accumulates all three products (xh·wh + xl·wh + xh·wl) into ONE column per centre
+// (A row [xh | xl | xh], B rows [wh | wh] and [wl]), otherwise hi and lo parts land in two
+// columns that the epilogue adds.
+template <int KP, int MB, int HW = 32, int AS = 0, bool K3 = false>
 struct TcTmem {
-  static constexpr int per = MB * 2 * KP;                                  // score columns per tile
-  static constexpr int acols = AS * MB * HW;                               // TS: A buffers (HW columns per row block)
+  static constexpr int per = MB * (K3 ? 1 : 2) * KP;                       // score columns per tile
+  static constexpr int ktail = (HW + 15) / 16;                             // K3: k-steps of the xh·wl tail
+  static constexpr int arow = K3 ? HW + 8 * ktail : HW;                    // A columns per row (TS)
+  static constexpr int acols = AS * MB * arow;                             // TS: A buffers
   static constexpr int NS0 = (512 - acols) / per;
   static constexpr int NS = NS0 >= 8 ? 8 : NS0;                            // TMEM score buffers
   static constexpr uint32_t a_base = NS * per;                             // first A column (TS)
@@ -518,7 +523,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   // A operand in TMEM (written by the transform with tcgen05.st, read by the MMA): takes the A
   // tile off shared memory (its stores and the MMA's operand reads) where the columns fit
   constexpr bool TS = tc_a_in_tmem<KP, TR>();
-  using TM = TcTmem<KP, MB, TcLayout<MP>::HW, TS ? TcStages<MP, KP>::a : 0>;
+  constexpr bool K3 = TS;  // one score column per centre (see TcTmem)
+  using TM = TcTmem<KP, MB, TcLayout<MP>::HW, TS ? TcStages<MP, KP>::a : 0, K3>;
+  constexpr int SC = K3 ? KP : 2 * KP;  // score columns per M block
   const bool resident = a.resident != 0;
   const TcSmem<MP, KP> S(MT > 0 ? MT : a.m, resident ? a.k : 0);
   constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
@@ -700,7 +707,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const int mj = warp - kMmaWarp;
       const uint32_t a0 = smem_u32(sm + S.off_a), w0 = smem_u32(s_w);
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform → uniform registers
-      constexpr uint32_t idesc = idesc_f16(2 * KP);
+      constexpr uint32_t idesc = idesc_f16(SC);
+      const uint64_t bdescL = make_desc(w0 + KP * 128, 16, 1024);  // B rows KP.. ([wl | 0]) for the K3 tail
       const uint64_t bdesc0 = make_desc(w0, 16, 1024);
       for (int i = (mj - (g0 & 1)) & 1; i < my_tiles && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
         const int g = g0 + i;
@@ -716,12 +724,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         if (elect_one()) {
 #pragma unroll
           for (int mb = 0; mb < MB; ++mb) {  // block mb: points 128·mb.. of the tile → columns mb·2KP..
-            const uint32_t dcol = tm + ss * TM::per + mb * 2 * KP;
+            const uint32_t dcol = tm + ss * TM::per + mb * SC;
             if constexpr (TS) {  // A from TMEM: 16 halfs = 8 columns per k-step
-              const uint32_t at = tm + TM::a_base + (uint32_t)(sa * L::HW);
+              const uint32_t at = tm + TM::a_base + (uint32_t)(sa * TM::arow);
 #pragma unroll
-              for (int ks = 0; ks < L::KSTEPS; ++ks)
+              for (int ks = 0; ks < L::KSTEPS; ++ks)  // [xh | xl] · [wh | wh]
                 mma_f16_ts(dcol, at + 8 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+              if constexpr (K3) {
+#pragma unroll
+                for (int ks = 0; ks < TM::ktail; ++ks)  // + xh · wl, same accumulator
+                  mma_f16_ts(dcol, at + L::HW + 8 * ks, bdescL + 2 * ks, idesc, 1u);
+              }
             } else {
               const uint64_t adesc0 = make_desc(a0 + sa * (TR * 128) + mb * (128 * 128), 16, 1024);
 #pragma unroll
@@ -801,9 +814,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           }
           if constexpr (TS) {
             // the point's A row [xh | xl] (HW 32-bit columns) → TMEM lane p of this tile's A buffer
-            const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + TM::a_base + (uint32_t)(sa * L::HW);
+            const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + TM::a_base + (uint32_t)(sa * TM::arow);
             tmem_st_row<L::HW / 2>(ta, hw);
             tmem_st_row<L::HW / 2>(ta + L::HW / 2, lw);
+            if constexpr (K3) {  // [xh | xl | xh | 0-pad to whole k-steps]
+              tmem_st_row<L::HW / 2>(ta + L::HW, hw);
+              if constexpr (TM::arow > L::HW + L::HW / 2) {
+                uint32_t z[TM::arow - L::HW - L::HW / 2];
+#pragma unroll
+                for (int c = 0; c < TM::arow - L::HW - L::HW / 2; ++c) z[c] = 0u;
+                tmem_st_row<TM::arow - L::HW - L::HW / 2>(ta + L::HW + L::HW / 2, z);
+              }
+            }
           } else {
             unsigned char* s_ab = s_a + mb * (128 * 128);
 #pragma unroll
@@ -890,7 +912,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           const int pp = p + 128 * mb;
           const bool active = pp < rows;
           const int old = olds[mb];
-          const uint32_t tcol = tmem + lane_base + ss * TM::per + mb * 2 * KP;
+          const uint32_t tcol = tmem + lane_base + ss * TM::per + mb * SC;
           // Certification: best = min score, candidates = {c : score ≤ best + E2}; the point is
           // certified iff the best is the only candidate (then it is the reference's argmin).
           // One packed counter per point: +1 per candidate, + c·2^8 (the index sum = the
@@ -903,11 +925,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           for (int ch = 0; ch < NCH; ++ch) {
             uint32_t r0[16], r1[16];
             tmem_ld16(tcol + ch * 16, r0);
-            tmem_ld16(tcol + KP + ch * 16, r1);
+            if constexpr (!K3) tmem_ld16(tcol + KP + ch * 16, r1);
             tmem_ld_wait();
 #pragma unroll
             for (int jj = 0; jj < 16; ++jj) {  // padded centres (c ≥ k) score +65504: never a candidate
-              const float v = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+              const float v = K3 ? __uint_as_float(r0[jj]) : __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
               vk[KEEP ? ch * 16 + jj : jj] = v;
             }
             if (a.dbg_scores != nullptr && active) {
@@ -932,10 +954,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             if (!KEEP) {
               uint32_t r0[16], r1[16];
               tmem_ld16(tcol + ch * 16, r0);
-              tmem_ld16(tcol + KP + ch * 16, r1);
+              if constexpr (!K3) tmem_ld16(tcol + KP + ch * 16, r1);
               tmem_ld_wait();
 #pragma unroll
-              for (int jj = 0; jj < 16; ++jj) vk[jj] = __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
+              for (int jj = 0; jj < 16; ++jj)
+                vk[jj] = K3 ? __uint_as_float(r0[jj]) : __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
             }
             uint32_t bits = 0;
 #pragma unroll
