@@ -75,7 +75,11 @@ __host__ __device__ constexpr bool tc_a_in_tmem() { return KM_A_IN_TMEM && KP <=
 
 template <int MP, int KP, int TR>
 struct TcBudget {
-  static constexpr int a = 2 * kTransformGroups;  // two A buffers per transform group (a group owns buffers g mod a)
+#ifndef KM_TS_ABUF
+#define KM_TS_ABUF 4
+#endif
+  // A buffers: per transform group (a group owns buffers g mod a); in TMEM they are cheap
+  static constexpr int a = (tc_a_in_tmem<KP, TR>() ? KM_TS_ABUF : 2) * kTransformGroups;
   static constexpr int mw = (KP + 31) / 32;
   static constexpr int raw_stride_max = ((TR * MP * 4 + 256 + 1023) / 1024) * 1024;
   static constexpr int fixed = (tc_a_in_tmem<KP, TR>() ? 0 : a * TR * 128) + 2 * KP * 128 +  // A ring, B tile
@@ -104,7 +108,7 @@ struct TcStages {
                                             TcBudget<MP, KP, 256>::raw_stride_max
                                       : TcBudget<MP, KP, 128>::raw;
   static constexpr int raw = raw_fit > 12 ? 12 : raw_fit;
-  static constexpr int a = 2 * kTransformGroups;
+  static constexpr int a = TcBudget<MP, KP, TR>::a;
   static_assert(raw >= 2, "shared-memory budget");
 };
 
