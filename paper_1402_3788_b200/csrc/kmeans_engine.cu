@@ -1118,8 +1118,8 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
   }
   const DevState s = *e->st_host;
   e->stats.passes += 1 + s.t - (s.converged ? 1 : 0);
-  e->stats.rechecked = (int64_t)s.rechecked;
-  e->stats.changed = (int64_t)s.changed;
+  e->stats.rechecked += (int64_t)s.rechecked;
+  e->stats.changed += (int64_t)s.changed;
   if (centers_out) CK(cudaMemcpyAsync(centers_out, e->cur, 8 * (size_t)k * e->m, cudaMemcpyDeviceToHost, e->stream));
   if (counts_out)  // converged: counts of the update; exhausted: the final finish folded bincount(L_T)
     CK(cudaMemcpyAsync(counts_out, e->model_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
