@@ -164,6 +164,18 @@ KM_API int km_step_fold(km_engine* e);
 KM_API int km_step_empty_list(km_engine* e, int32_t* empties_out, int32_t* n_out);
 KM_API int km_step_label_of(km_engine* e, int64_t local_row, int32_t* label_out);
 KM_API int km_step_check(km_engine* e, double tol, int32_t* converged_out);
+
+/* Batched form of the same loop (no host round trip per iteration): after km_step_begin and
+ * km_step_loop_begin, enqueue km_step_loop_pass (L0), then per iteration [allreduce of the
+ * partial buffer, km_step_loop_finish, km_step_loop_pass]; read {t, done, converged, need_host}
+ * with km_step_loop_state every few iterations.  Kernels are gated on the device state, so
+ * iterations enqueued past the end do no work.  need_host: run the global repair with the
+ * km_step_repair_* calls, then km_step_loop_check. */
+KM_API int km_step_loop_begin(km_engine* e, int32_t max_iters, double tol);
+KM_API int km_step_loop_pass(km_engine* e);
+KM_API int km_step_loop_finish(km_engine* e);
+KM_API int km_step_loop_check(km_engine* e);
+KM_API int km_step_loop_state(km_engine* e, int32_t* out4);
 KM_API int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, int64_t* labels_out);
 
 KM_API int km_get_stats(km_engine* e, km_stats* out);

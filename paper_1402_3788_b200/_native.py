@@ -71,6 +71,11 @@ SIGNATURES = {
     "km_wcss": (ctypes.c_int, [P, P, I32, P, ctypes.POINTER(F64)]),
     "km_center_distances": (ctypes.c_int, [P, P, I32, P]),
     "km_diameter": (ctypes.c_int, [P, I64, ctypes.POINTER(F64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+    "km_step_loop_begin": (ctypes.c_int, [P, I32, F64]),
+    "km_step_loop_pass": (ctypes.c_int, [P]),
+    "km_step_loop_finish": (ctypes.c_int, [P]),
+    "km_step_loop_check": (ctypes.c_int, [P]),
+    "km_step_loop_state": (ctypes.c_int, [P, P]),
     "km_seed_reset": (ctypes.c_int, [P]),
     "km_seed_add": (ctypes.c_int, [P, I64, ctypes.POINTER(F64), ctypes.POINTER(I64)]),
     "km_seed_min_d2": (ctypes.c_int, [P, I64, ctypes.POINTER(F64)]),
@@ -236,6 +241,25 @@ class NativeEngine:
         out = np.empty((self.n, centers.shape[0]), dtype=np.float64)
         self._check(self._lib.km_center_distances(self._h, _ptr(centers), centers.shape[0], _ptr(out)))
         return out
+
+    # -- batched step loop (multi-GPU driver without a host round trip per iteration) --
+    def loop_begin(self, max_iters, tol):
+        self._check(self._lib.km_step_loop_begin(self._h, int(max_iters), float(tol)))
+
+    def loop_pass(self):
+        self._check(self._lib.km_step_loop_pass(self._h))
+
+    def loop_finish(self):
+        self._check(self._lib.km_step_loop_finish(self._h))
+
+    def loop_check(self):
+        self._check(self._lib.km_step_loop_check(self._h))
+
+    def loop_state(self):
+        """(t, done, converged, need_host) — one device→host read."""
+        out = np.zeros(4, dtype=np.int32)
+        self._check(self._lib.km_step_loop_state(self._h, _ptr(out)))
+        return int(out[0]), bool(out[1]), bool(out[2]), bool(out[3])
 
     # -- seeding (SURVEY §8f #1) -------------------------------------------------
     def diameter(self, pair_cap=None):

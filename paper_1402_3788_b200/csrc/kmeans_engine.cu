@@ -1478,6 +1478,51 @@ int km_step_empty_list(km_engine* e, int32_t* empties_out, int32_t* n_out) {
   return KM_OK;
 }
 
+// Batched step loop: the device keeps the loop state (DevState) exactly as km_lloyd does, so a
+// driver can enqueue [allreduce, finish, pass] for several iterations and read the state once.
+int km_step_loop_begin(km_engine* e, int32_t max_iters, double tol) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->part) return set_err(e, KM_ERR_CONTRACT, "call km_step_begin first");
+  if (max_iters < 1) return set_err(e, KM_ERR_CONTRACT, "max_iters must be >= 1, got %d", max_iters);
+  if (!(tol >= 0.0)) return set_err(e, KM_ERR_CONTRACT, "tol must be >= 0, got %g", tol);
+  cudaSetDevice(e->device);
+  return reset_state(e, max_iters, tol);
+}
+
+int km_step_loop_pass(km_engine* e) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->part) return set_err(e, KM_ERR_CONTRACT, "call km_step_begin first");
+  cudaSetDevice(e->device);
+  return launch_pass(e, PASS_ASSIGN_SUMS, true);  // gated: no work once done / waiting for the host
+}
+
+int km_step_loop_finish(km_engine* e) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->part) return set_err(e, KM_ERR_CONTRACT, "call km_step_begin first");
+  cudaSetDevice(e->device);
+  return launch_finish(e, 0, !e->last_pass_full);  // engine.iterate's update/test/exhaustion rules
+}
+
+int km_step_loop_check(km_engine* e) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  return launch_check(e);  // after a host repair: congruence test, filter prep, exhaustion
+}
+
+int km_step_loop_state(km_engine* e, int32_t* out4) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if ((r = read_state(e))) return r;
+  if (out4) {
+    out4[0] = e->st_host->t;
+    out4[1] = e->st_host->done;
+    out4[2] = e->st_host->converged;
+    out4[3] = e->st_host->need_host;
+  }
+  return KM_OK;
+}
+
 int km_step_check(km_engine* e, double tol, int32_t* converged_out) {
   if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
   cudaSetDevice(e->device);

@@ -127,6 +127,8 @@ def run_sharded(engine, coll, c0, max_iters=1000, tol=0.0, want_labels=True) -> 
     engine.set_frac_bits(engine.frac_bits_for(absmax, n_total))  # one global fixed-point scale
     engine.step_begin(c0)
     part = partials_tensor(engine)
+    if hasattr(engine, "loop_begin"):  # device-state loop: a few iterations per host round trip
+        return _run_batched(engine, coll, part, k, max_iters, tol, want_labels, row_offset)
     engine.step_pass()                       # L0 = A(C0) + its sums
     t = 0
     converged = False
@@ -148,6 +150,36 @@ def run_sharded(engine, coll, c0, max_iters=1000, tol=0.0, want_labels=True) -> 
         engine.step_pass()
     centers, counts, labels = engine.step_read(k, want_labels=want_labels)
     return ShardResult(centers, counts, labels, t, converged, row_offset)
+
+
+def _run_batched(engine, coll, part, k, max_iters, tol, want_labels, row_offset) -> ShardResult:
+    """The same loop with the device holding the state (DevState, as km_lloyd does): iterations
+    are enqueued in batches of up to 16 [allreduce, finish, pass] and the state is read once per
+    batch.  Kernels are gated on the state, so iterations enqueued past the end do no work and
+    the allreduces then sum zeros.  Every rank reads the same state (replicated totals)."""
+    engine.loop_begin(max_iters, tol)
+    engine.loop_pass()                       # L0 = A(C0) + its sums
+    batch = 1
+    while True:
+        for _ in range(batch):
+            coll.allreduce_sum_(part)        # the one collective per iteration
+            engine.loop_finish()             # update, empties, congruence, exhaustion (device)
+            engine.loop_pass()               # next assignment (gated)
+        t, done, conv, need_host = engine.loop_state()
+        if done:
+            break
+        if need_host:                        # empty clusters: the global repair, then the test
+            _global_repair(engine, coll, k, row_offset)
+            engine.loop_check()
+            t, done, conv, _ = engine.loop_state()
+            if done:
+                break
+            engine.loop_pass()               # the assignment with the repaired centres
+            batch = 1
+            continue
+        batch = min(batch * 2, 16)
+    centers, counts, labels = engine.step_read(k, want_labels=want_labels)
+    return ShardResult(centers, counts, labels, t, conv, row_offset)
 
 
 def shard_rows(n: int, world: int, rank: int):

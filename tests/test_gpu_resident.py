@@ -84,3 +84,49 @@ def test_resident_exhausted_counts_are_final_assignment():
         assert it == iters and not conv and not want["converged"]
         assert np.array_equal(labels, want["labels"]) and np.array_equal(counts, want["counts"])
         assert np.array_equal(np.bincount(labels, minlength=16), counts)
+
+
+def test_sharded_nccl_world1_equals_resident():
+    """The multi-GPU driver (row shards, NCCL allreduce, batched device-state loop) at world size 1
+    must reproduce the single-GPU resident loop bit for bit — including a repair and exhaustion."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1402_3788_b200 import _native
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+    from paper_1402_3788_b200.distributed import TorchCollective, run_sharded
+
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        coll = TorchCollective()
+        x = generate_synthetic_array(150_000, 25, 16, seed=9, dtype=np.float32)
+        for c0, iters in ((x[:16].astype(np.float64), 1000), (x[:16].astype(np.float64), 9)):
+            want = fit(x, c0, iters)
+            eng = _native.NativeEngine(0)
+            eng.load(x)
+            got = run_sharded(eng, coll, c0, max_iters=iters)
+            eng.close()
+            assert got.iterations == want[3] and got.converged == want[4]
+            assert np.array_equal(got.centers, want[0]) and np.array_equal(got.counts, want[1])
+            assert np.array_equal(got.labels, want[2])
+        c0 = x[:16].astype(np.float64)
+        c0[7] = c0[2]  # an empty cluster after the first update: global repair through the collective
+        want = fit(x, c0, 300)
+        eng = _native.NativeEngine(0)
+        eng.load(x)
+        got = run_sharded(eng, coll, c0, max_iters=300)
+        eng.close()
+        assert want[5]["repairs"] >= 1
+        assert got.iterations == want[3] and got.converged == want[4]
+        assert np.array_equal(got.labels, want[2]) and np.array_equal(got.counts, want[1])
+        assert np.array_equal(got.centers, want[0])
+    finally:
+        dist.destroy_process_group()
