@@ -1500,7 +1500,12 @@ int km_step_loop_finish(km_engine* e) {
   if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
   if (!e->part) return set_err(e, KM_ERR_CONTRACT, "call km_step_begin first");
   cudaSetDevice(e->device);
-  return launch_finish(e, 0, !e->last_pass_full);  // engine.iterate's update/test/exhaustion rules
+  if (e->m > 32) return launch_finish(e, 0, !e->last_pass_full);  // engine.iterate's update/test/exhaustion rules
+  FinishArgs f = finish_args(e, 0, !e->last_pass_full);
+  lloyd_finish_warp_kernel<<<1, 512, 0, e->stream>>>(f);
+  CK_LAUNCH("lloyd_finish_warp_kernel launch");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
 }
 
 int km_step_loop_check(km_engine* e) {

@@ -284,6 +284,115 @@ __global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a, int sta
 }
 
 
+// The loop finish (finish_block mode 0, same decisions) for m ≤ 32 with warp per centre and lane
+// per feature: fold Δ, C_t = S/N, empties, the congruence test and the filter operands in one
+// parallel pass — the single-CTA serial chains of finish_block cost ~10 µs per iteration.
+__global__ void __launch_bounds__(512) lloyd_finish_warp_kernel(FinishArgs a) {
+  DevState* st = a.st;
+  const int k = a.k, m = a.m, km = k * m;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  if (st->done || st->need_host) return;
+  __shared__ int s_flags[32];
+  __shared__ float s_max[32];
+  if (tid == 0 && a.recheck_count) {
+    st->rechecked += *a.recheck_count;
+    *a.recheck_count = 0u;
+  }
+  // running totals of the current labels (exact integer arithmetic)
+  for (int i = tid; i < km + k; i += blockDim.x) {
+    a.tot[i] = a.accumulate ? a.tot[i] + a.part[i] : a.part[i];
+    a.part[i] = 0ull;
+  }
+  __syncthreads();
+  const unsigned long long* cnts = a.tot + km;
+  if (st->exhausted) {  // the final assign pass of an exhausted run: counts = bincount(L_T)
+    for (int c = tid; c < k; c += blockDim.x) a.model_counts[c] = (long long)cnts[c];
+    if (tid == 0) st->done = 1;
+    return;
+  }
+  const double tol = st->tol;
+  const int hw = 8 * ((m + 1 + 7) / 8);
+  int flags = 0;   // bit 0: some cluster empty, bit 1: some centre moved
+  float wmax = 0.f;
+  for (int c = warp; c < k; c += nw) {
+    const long long nc = (long long)cnts[c];
+    const bool fv = lane < m;
+    const long long sv = fv ? (long long)a.tot[(size_t)c * m + lane] : 0ll;
+    const double v = (fv && nc > 0) ? __ddiv_rn(__dmul_rn((double)sv, a.inv_scale), (double)nc) : 0.0;
+    const double vo = fv ? a.cur[(size_t)c * m + lane] : 0.0;
+    if (fv) {
+      a.prev[(size_t)c * m + lane] = vo;
+      a.cur[(size_t)c * m + lane] = v;
+    }
+    if (lane == 0) a.model_counts[c] = nc;
+    const double dd = fv ? __dmul_rn(__dsub_rn(vo, v), __dsub_rn(vo, v)) : 0.0;
+    bool moved;
+    if (tol == 0.0) {
+      moved = __any_sync(0xffffffffu, dd != 0.0);
+    } else {
+      double acc = 0.0;  // the reference order: features ascending
+      for (int f = 0; f < m; ++f) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, dd, f));
+      moved = !(sqrt(acc) <= tol);
+    }
+    flags |= (nc == 0 ? 1 : 0) | (moved ? 2 : 0);
+    // filter operands: ‖fl32(c)‖² (fp64, exact squares), max ‖c‖, SIMT w / cn, tensor-core rows
+    const float v32 = __double2float_rn(v);
+    const double q = fv ? (double)v32 : 0.0;
+    double cn2 = q * q;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cn2 += __shfl_xor_sync(0xffffffffu, cn2, o);
+    wmax = fmaxf(wmax, __double2float_ru(sqrt(cn2) * (1.0 + 1e-12)));
+    if (lane == 0) a.cn[c] = __double2float_rn(cn2);
+    for (int f = lane; f < a.mpad; f += 32) a.w[(size_t)c * a.mpad + f] = (f < m) ? -2.0f * v32 : 0.0f;
+    if (a.wop != nullptr) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int col = lane + 32 * h;
+        const int f = col < hw ? col : col - hw;
+        const double vf = __shfl_sync(0xffffffffu, v, f < 32 ? f : 0);
+        float w = 0.f;
+        if (col < 2 * hw) {
+          if (f < m) w = -2.0f * __double2float_rn(vf) * a.pre;
+          else if (f == m) w = __double2float_rn(cn2 * (double)a.pre * (double)a.pre);
+        }
+        const __half wh = __float2half_rn(w);
+        const __half wl = __float2half_rn(w - __half2float(wh));
+        a.wop[(size_t)c * 64 + col] = (col < 2 * hw) ? __half_as_ushort(wh) : (unsigned short)0;
+        a.wop[(size_t)(a.kp + c) * 64 + col] = (col < hw) ? __half_as_ushort(wl) : (unsigned short)0;
+      }
+    }
+  }
+  if (lane == 0) {
+    s_flags[warp] = flags;
+    s_max[warp] = wmax;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int fl = 0;
+    float mx = 0.f;
+    for (int w = 0; w < nw; ++w) {
+      fl |= s_flags[w];
+      mx = fmaxf(mx, s_max[w]);
+    }
+    st->t += 1;
+    int ne = 0;
+    for (int c = 0; c < k; ++c) ne += (cnts[c] == 0ull);
+    st->n_empty = ne;
+    if (fl & 1) {
+      st->need_host = 1;  // empty clusters: the host repairs, then the check kernel runs the test
+    } else {
+      a.cmax[0] = mx;
+      st->need_host = 0;
+      if (!(fl & 2)) {
+        st->converged = 1;
+        st->done = 1;
+      } else if (st->t >= st->max_iters) {
+        st->exhausted = 1;  // reference: assignment = assign_fn(model) once more, then return
+      }
+    }
+  }
+}
+
 // After a host-driven repair: congruence test + prep (no division).
 __global__ void __launch_bounds__(512) lloyd_check_kernel(FinishArgs a) {
   __shared__ float s_red[32];
