@@ -26,10 +26,11 @@
 //
 // Warp roles (persistent CTA, one per SM), pipelined over 128-point tiles:
 //   warps 0-7  : transform   two groups, alternate tiles: raw tile → fp16 [hi|lo] A operand
-//   warps 8-15 : epilogue    two groups, alternate tiles: TMEM scores → top-2 →
+//   warps 8-19 : epilogue    three groups, round-robin tiles (two when the TMEM score ring is
+//                            shallower than 6 buffers, KP > 32): TMEM scores → top-2 →
 //                            certify → Δ update (thread = point = TMEM lane)
-//   warp 16    : TMA producer (cp.async.bulk 1-D copies of raw 4·m-byte rows)
-//   warp 17    : TMEM allocator + single-thread MMA issuer
+//   warp 20    : TMA producer (cp.async.bulk 1-D copies of raw 4·m-byte rows)
+//   warps 21-22: TMEM allocator + MMA issuers (alternate tiles); warp 23: recheck
 #pragma once
 #include <cuda_runtime.h>
 #include <cuda_fp16.h>
@@ -52,7 +53,7 @@ constexpr int kTileRows = 128;
 constexpr int kTransformGroups = KM_TRANSFORM_GROUPS;  // transform warpgroups (tile g → group g mod groups)
 constexpr int kTransformWarps = 4 * kTransformGroups;
 #ifndef KM_EPI_GROUPS
-#define KM_EPI_GROUPS 2
+#define KM_EPI_GROUPS 3
 #endif
 constexpr int kEpiGroups = KM_EPI_GROUPS;          // epilogue warpgroups (tile g → group g mod kEpiGroups)
 constexpr int kEpiWarps = 4 * kEpiGroups;
@@ -530,6 +531,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   constexpr bool K3 = TS;  // one score column per centre (see TcTmem)
   using TM = TcTmem<KP, MB, TcLayout<MP>::HW, TS ? TcStages<MP, KP>::a : 0, K3>;
   constexpr int SC = K3 ? KP : 2 * KP;  // score columns per M block
+  // Active epilogue groups.  A group waiting on tile g must know that the previous fill of the
+  // score buffer (tile g − NS) has completed, or the parity wait aliases: it has consumed tiles
+  // g − EG, g − 2·EG, …, and a consumed tile issued by the same MMA warp as g (same parity) at or
+  // after g − NS implies it (tcgen05.commit covers every earlier MMA of that thread).  So NS must
+  // reach the first even multiple of EG; narrower score rings (KP > 32) run two groups and the
+  // third idles.
+  constexpr int EG = TM::NS % 2 == 0 && TM::NS >= (kEpiGroups % 2 ? 2 * kEpiGroups : kEpiGroups) ? kEpiGroups : 2;
   const bool resident = a.resident != 0;
   const TcSmem<MP, KP> S(MT > 0 ? MT : a.m, resident ? a.k : 0);
   constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
@@ -876,16 +884,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const int64_t r = (t_lo + i) * TR + 128 * mb + p;
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
-      const int i0 = ((e - g0) % kEpiGroups + kEpiGroups) % kEpiGroups;
+      const int i0 = e < EG ? ((e - g0) % EG + EG) % EG : my_tiles;  // groups ≥ EG idle
       // previous labels prefetched two tiles of this group ahead (an L2 or DRAM round trip
       // must not stall the epilogue)
       int old_n1[MB], old_n2[MB];
 #pragma unroll
       for (int mb = 0; mb < MB; ++mb) {
         old_n1[mb] = prev_label(i0, mb);
-        old_n2[mb] = prev_label(i0 + kEpiGroups, mb);
+        old_n2[mb] = prev_label(i0 + EG, mb);
       }
-      for (int i = i0; i < my_tiles && !(KM_DBG_FLAGS & 4); i += kEpiGroups) {
+      for (int i = i0; i < my_tiles && !(KM_DBG_FLAGS & 4); i += EG) {
         const int g = g0 + i;
         const int ss = g % TM::NS;
         const int64_t row0 = (t_lo + i) * TR;
@@ -896,7 +904,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         for (int mb = 0; mb < MB; ++mb) {
           olds[mb] = old_n1[mb];
           old_n1[mb] = old_n2[mb];
-          old_n2[mb] = prev_label(i + 2 * kEpiGroups, mb);
+          old_n2[mb] = prev_label(i + 2 * EG, mb);
         }
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;

@@ -142,7 +142,7 @@ def test_iterate_seam_with_device_steps():
 
 @pytest.mark.parametrize("n,m,k,iters", [(100_000, 10, 8, 1000), (200_000, 25, 16, 40), (50_000, 25, 64, 15),
                                          (20_000, 7, 33, 25), (4_099, 3, 5, 1000), (1_000, 70, 6, 30),
-                                         (30_000, 25, 512, 4)])
+                                         (30_000, 25, 512, 4), (400_000, 25, 64, 6), (400_000, 25, 128, 4)])
 def test_vs_oracle_seeded(native, n, m, k, iters):
     from oracle import oracle
     from paper_1402_3788_b200.datasets import generate_synthetic_array
@@ -196,7 +196,8 @@ def test_deterministic_bits(native):
 # --- full BASELINE sizes: size-independent properties ------------------------------------------
 
 
-@pytest.mark.parametrize("n,m,k,iters", [(2_000_000, 25, 16, 12), (2_000_000, 25, 512, 2)])
+@pytest.mark.parametrize("n,m,k,iters", [(2_000_000, 25, 16, 12), (2_000_000, 25, 64, 5), (2_000_000, 25, 128, 4),
+                                         (2_000_000, 25, 512, 2)])
 def test_full_size_properties(native, n, m, k, iters):
     """At BASELINE sizes: (1) the labels are the reference argmin for the
     returned centres (checked with the oracle on a 20k-row sample),
