@@ -186,6 +186,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 #endif
 }
+// Wait of a role that is normally ahead of its producer (the epilogue on the MMA): a failed
+// try_wait returns on any barrier event of the CTA, so with 12 epilogue warps waiting the retry
+// loop would take a quarter of the SM's issue slots away from the transform; back off instead.
+#ifndef KM_EPI_SLEEP
+#define KM_EPI_SLEEP 0
+#endif
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+#if KM_EPI_SLEEP > 0
+  uint32_t n = 0;
+  while (!mbar_try(bar, parity)) {
+    __nanosleep(KM_EPI_SLEEP);
+    if (++n == (1u << 26)) __trap();
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
@@ -517,6 +534,67 @@ __device__ __forceinline__ int exact_candidates(const float* __restrict__ gx, in
 //   the first tiles of pass t+1 while the tail, the barrier and the finish run.  Stops
 //   on convergence, after the final assign pass of an exhausted run, or on empty
 //   clusters (the host repairs them and relaunches).
+// Exact incremental update of the per-cluster fixed-point sums for the changed points of one warp
+// (`pend`: lanes whose label changed; lane l holds point wrow0 + l, new label bi, old label old).
+// Out of line so its registers do not weigh on the steady-state epilogue, where changes are rare.
+//  * sparse (steady state): warp-cooperative, four changed points at a time: lane f loads
+//    feature f of each (one coalesced L2 round trip per batch, the rows were just streamed) and
+//    adds it to the new cluster / subtracts it from the old one; lane m moves the counts;
+//  * the first pass (every point adds its row): thread per point, loads batched ahead of the
+//    atomics.
+static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int m, int64_t wrow0, int lane, int bi, int old,
+                                        unsigned int pend, bool full, unsigned long long* s_acc, int km,
+                                        float scale_f, double scale_d, bool use_dscale) {
+  auto fixed = [&](float xv) -> long long {
+    return use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d)) : __float2ll_rn(__fmul_rn(xv, scale_f));
+  };
+  if (full) {
+    if (!((pend >> lane) & 1u)) return;
+    const float* xr = x + (wrow0 + lane) * m;
+    constexpr int CH = 8;
+    for (int f0 = 0; f0 < m; f0 += CH) {
+      float xv[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) xv[j] = (f0 + j < m) ? __ldg(xr + f0 + j) : 0.f;
+#pragma unroll
+      for (int j = 0; j < CH; ++j) {
+        if (f0 + j < m) {
+          const long long v = fixed(xv[j]);
+          smem_add64(s_acc + (size_t)bi * m + f0 + j, (unsigned long long)v);
+          if (old >= 0) smem_add64(s_acc + (size_t)old * m + f0 + j, (unsigned long long)(-v));
+        }
+      }
+    }
+    smem_add64(s_acc + (size_t)km + bi, 1ull);
+    if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+    return;
+  }
+  while (pend) {
+    int src[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      src[j] = pend ? __ffs(pend) - 1 : -1;
+      if (pend) pend &= pend - 1;
+    }
+    float xv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xv[j] = (src[j] >= 0 && lane < m) ? __ldg(x + (wrow0 + src[j]) * m + lane) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (src[j] < 0) break;
+      const int nb = __shfl_sync(0xffffffffu, bi, src[j]), ob = __shfl_sync(0xffffffffu, old, src[j]);
+      if (lane < m) {
+        const long long v = fixed(xv[j]);
+        smem_add64(s_acc + (size_t)nb * m + lane, (unsigned long long)v);
+        if (ob >= 0) smem_add64(s_acc + (size_t)ob * m + lane, (unsigned long long)(-v));
+      } else if (lane == m) {
+        smem_add64(s_acc + (size_t)km + nb, 1ull);
+        if (ob >= 0) smem_add64(s_acc + (size_t)km + ob, ~0ull);
+      }
+    }
+  }
+}
+
 template <int MT, int KP, bool PRE>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
   static_assert(kThreadsTC == (kTransformWarps + kEpiWarps + 4) * 32, "warp-role layout");
@@ -909,7 +987,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[4] = clock64();
-        mbar_wait(s_full + ss, (g / TM::NS) & 1);
+        mbar_wait_backoff(s_full + ss, (g / TM::NS) & 1);
         if (stamp) ts[5] = clock64();
         tc_fence_after();
         if (KM_DBG_FLAGS & 32) {  // timing experiment only: no epilogue work (labels unchanged)
@@ -1014,22 +1092,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
           const int bi = bis[mb], old = olds[mb];
-          if (bi != old) {
-            // --- exact incremental update of the per-cluster fixed-point sums
-            const int64_t row = row0 + 128 * mb + p;
+          // --- exact incremental update of the per-cluster fixed-point sums (delta_rows)
+          const bool chg = bi != old;
+          if (chg) {
             ++my_changed;
-            a.labels[row] = bi;
-            const float* xr = a.x + row * m;  // just streamed: L2 hit
-            for (int f = 0; f < m; ++f) {
-              const float xv = __ldg(xr + f);
-              const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d))
-                                             : __float2ll_rn(__fmul_rn(xv, scale_f));
-              smem_add64(s_acc + (size_t)bi * m + f, (unsigned long long)v);
-              if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
-            }
-            smem_add64(s_acc + (size_t)km + bi, 1ull);
-            if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+            a.labels[row0 + 128 * mb + p] = bi;
           }
+          const unsigned int pend = __ballot_sync(0xffffffffu, chg);
+          if (pend)
+            delta_rows(a.x, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, s_acc, km, scale_f, scale_d,
+                       use_dscale);
         }
         if (stamp) ts[6] = clock64();
       }
