@@ -136,6 +136,22 @@ KM_API int km_seed_reset(km_engine* e);
 KM_API int km_seed_add(km_engine* e, int64_t c, double* max_v, int64_t* max_i);
 KM_API int km_seed_min_d2(km_engine* e, int64_t i, double* out);
 
+/* ---- device jobs (the reference's offload-device protocol) ----
+ * The B200 side of a `Device._execute(job)` (device.py:153-239) for the three job kinds:
+ * km_max_pair_rows: MAX_PAIR (device.max_pair_job :117-122 → _kernels.max_pair_rows,
+ *   _kernels.py:48-81): best pair over the given strictly ascending rows × columns j > i, exact
+ *   fp64 d² (not its root), ties → smallest (i, j); (-1, -1, -1) when the rows give no pair.
+ * km_block_sums: COORD_SUM (labels == NULL; sums_out (nb, m)) and CLUSTER_SUM (sums_out
+ *   (nb, k, m), counts_out (nb, k)) over samples [start, stop), start on a `block` boundary
+ *   (device._check_range :139-150, HostReferenceDevice._execute :218-239 →
+ *   _kernels.coord_sums_block / cluster_sums_block, _kernels.py:84-113); nb = ceil((stop −
+ *   start)/block).  A label outside [0, k) → KM_ERR_VALIDATION with *bad_out = its sample index
+ *   (device.py:233-238).  Sums are exact fixed point rounded once to fp64. */
+KM_API int km_max_pair_rows(km_engine* e, const int64_t* rows, int64_t nrows, double* d2_out, int64_t* i_out,
+                            int64_t* j_out);
+KM_API int km_block_sums(km_engine* e, const int64_t* labels, int32_t k, int64_t start, int64_t stop, int64_t block,
+                         double* sums_out, int64_t* counts_out, int64_t* bad_out);
+
 /* ---- row-sharded multi-GPU step API (partition.py:84-100,237-261) ------
  * One process per GPU holds a contiguous row shard.  Per iteration:
  *   km_step_pass      fused assign + per-cluster fixed-point sums of the shard

@@ -53,6 +53,8 @@ def _load():
     lib.ko_iterate.argtypes = [P, I, I, P, I, I, ctypes.c_double, I, ctypes.c_int, P, P, P,
                                ctypes.POINTER(ctypes.c_int)]
     lib.ko_iterate.restype = I
+    lib.ko_cluster_sums_block.argtypes = [P, I, P, I, I, I, P, P]
+    lib.ko_cluster_sums_block.restype = I
     _lib = lib
     return lib
 
@@ -182,6 +184,45 @@ def diameter(coords, pair_cap=None):
             if d2[jj] > best:
                 best, bi, bj = float(d2[jj]), int(i), int(i + 1 + jj)
     return float(np.sqrt(best)), bi, bj
+
+
+def max_pair_rows(coords, rows):
+    """_kernels.max_pair_rows (_kernels.py:48-81) over an explicit ascending row list (the
+    MAX_PAIR device job, device.py:204-216): (d2, i, j), (-1.0, -1, -1) when no pair."""
+    x = _f64(coords)
+    best, bi, bj = -1.0, -1, -1
+    for i in np.asarray(rows, dtype=np.int64):
+        rest = x[i + 1:]
+        d2 = np.zeros(rest.shape[0])
+        for f in range(x.shape[1]):
+            d = x[i, f] - rest[:, f]
+            d2 += d * d
+        if d2.size:
+            jj = int(np.argmax(d2))
+            if d2[jj] > best:
+                best, bi, bj = float(d2[jj]), int(i), int(i + 1 + jj)
+    return best, bi, bj
+
+
+def block_sums(coords, start, stop, block, labels=None, k=1):
+    """HostReferenceDevice._execute sum jobs (device.py:218-239): per-block sequential fp64 sums
+    (_kernels.cluster_sums_block, _kernels.py:97-113; coord_sums_block = every label 0).
+    Returns (sums, counts, bad) with bad = the first out-of-range sample or -1."""
+    lib = _load()
+    x = _f64(coords)
+    n, m = x.shape
+    lab = np.zeros(n, dtype=np.int64) if labels is None else np.ascontiguousarray(labels, dtype=np.int64)
+    kk = 1 if labels is None else int(k)
+    bounds = [(s, min(s + block, stop)) for s in range(start, stop, block)]
+    sums = np.zeros((len(bounds), kk, m))
+    counts = np.zeros((len(bounds), kk), dtype=np.int64)
+    for b, (s, e) in enumerate(bounds):
+        bad = lib.ko_cluster_sums_block(_ptr(x), m, _ptr(lab), kk, s, e, _ptr(sums[b]), _ptr(counts[b]))
+        if bad >= 0:
+            return None, None, int(bad)
+    if labels is None:
+        return sums[:, 0, :], None, -1
+    return sums, counts, -1
 
 
 def _lower_min_d2(x, c, min_d2):

@@ -71,6 +71,8 @@ SIGNATURES = {
     "km_wcss": (ctypes.c_int, [P, P, I32, P, ctypes.POINTER(F64)]),
     "km_center_distances": (ctypes.c_int, [P, P, I32, P]),
     "km_diameter": (ctypes.c_int, [P, I64, ctypes.POINTER(F64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+    "km_max_pair_rows": (ctypes.c_int, [P, P, I64, ctypes.POINTER(F64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
+    "km_block_sums": (ctypes.c_int, [P, P, I32, I64, I64, I64, P, P, ctypes.POINTER(I64)]),
     "km_step_loop_begin": (ctypes.c_int, [P, I32, F64]),
     "km_step_loop_pass": (ctypes.c_int, [P]),
     "km_step_loop_finish": (ctypes.c_int, [P]),
@@ -268,6 +270,34 @@ class NativeEngine:
         cap = 0 if pair_cap is None else int(pair_cap)
         self._check(self._lib.km_diameter(self._h, cap, ctypes.byref(d), ctypes.byref(i), ctypes.byref(j)))
         return d.value, i.value, j.value
+
+    # -- device jobs (device.py:117-239) ----------------------------
+    def max_pair_rows(self, rows):
+        """MAX_PAIR job: (d2, i, j) over the ascending `rows` × columns j > i; (-1.0, -1, -1) if none."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        d2, i, j = F64(), I64(), I64()
+        self._check(self._lib.km_max_pair_rows(self._h, _ptr(rows), rows.shape[0], ctypes.byref(d2),
+                                               ctypes.byref(i), ctypes.byref(j)))
+        return d2.value, i.value, j.value
+
+    def block_sums(self, start, stop, block, labels=None, k=0):
+        """COORD_SUM (labels None): (nb, m) sums.  CLUSTER_SUM: ((nb, k, m) sums, (nb, k) counts).
+        A label outside [0, k) raises ValidationFailureError naming the first such sample."""
+        nb = -(-(int(stop) - int(start)) // int(block)) if stop > start else 0
+        bad = I64(-1)
+        if labels is None:
+            sums = np.zeros((nb, self.m), dtype=np.float64)
+            self._check(self._lib.km_block_sums(self._h, None, 1, int(start), int(stop), int(block), _ptr(sums),
+                                                None, ctypes.byref(bad)))
+            return sums, None
+        labels = np.ascontiguousarray(labels, dtype=np.int64)
+        if labels.shape[0] < stop:
+            raise ContractViolationError(f"labels cover {labels.shape[0]} samples, job needs {stop}")
+        sums = np.zeros((nb, int(k), self.m), dtype=np.float64)
+        counts = np.zeros((nb, int(k)), dtype=np.int64)
+        self._check(self._lib.km_block_sums(self._h, _ptr(labels), int(k), int(start), int(stop), int(block),
+                                            _ptr(sums), _ptr(counts), ctypes.byref(bad)))
+        return sums, counts
 
     def seed_reset(self):
         self._check(self._lib.km_seed_reset(self._h))

@@ -45,6 +45,11 @@ struct km_engine {
   double* seed_pv = nullptr;
   long long* seed_pi = nullptr;
   size_t pair_best_cap = 0, seed_pv_cap = 0, seed_pi_cap = 0;
+  // device jobs (MAX_PAIR rows, COORD_SUM / CLUSTER_SUM per-block sums)
+  void* rows_dev = nullptr;
+  void* job_acc = nullptr;
+  void* job_lab = nullptr;
+  size_t rows_cap = 0, job_acc_cap = 0, job_lab_cap = 0;
   bool seed_ready = false;
   int64_t n = 0;
   int32_t m = 0;
@@ -772,6 +777,7 @@ int km_destroy(km_engine* e) {
   dfree(e->xbuf); dfree(e->stage); dfree(e->labels); dfree(e->recheck_rows); dfree(e->d2);
   dfree(e->labels64); dfree(e->partials);
   dfree(e->pair_best); dfree(e->seed_pv); dfree(e->seed_pi);
+  dfree(e->rows_dev); dfree(e->job_acc); dfree(e->job_lab);
   for (cudaEvent_t ev : e->ev) cudaEventDestroy(ev);
   dfree(e->st);
   dfree(e->scratch_u);
@@ -1171,21 +1177,11 @@ int km_wcss(km_engine* e, const double* centers, int32_t k, const int64_t* label
 // ---------------------------------------------------------------------------
 // Seeding: diameter pair scan + maximin / random-far primitives
 // ---------------------------------------------------------------------------
-int km_diameter(km_engine* e, int64_t pair_cap, double* d_out, int64_t* i_out, int64_t* j_out) {
-  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
-  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
-  cudaSetDevice(e->device);
+// Best pair (largest exact d², then smallest i, then smallest j) over scan rows × columns j > i:
+// rows r·stride for r < R, or rows[r] (device, ascending) when given.  best.i < 0: no pair.
+static int pair_scan_best(km_engine* e, int64_t stride, int64_t R, const long long* rows, PairBest* best_out) {
   const int64_t n = e->n;
   const int m = e->m;
-  if (n < 2) return set_err(e, KM_ERR_CONTRACT, "diameter needs at least 2 samples, got %lld", (long long)n);
-  // engine.scan_rows (engine.py:124-138): every row, or every stride-th row under a pair cap
-  const unsigned __int128 total = (unsigned __int128)n * (unsigned __int128)(n - 1) / 2;
-  int64_t stride = 1;
-  if (pair_cap > 0 && total > (unsigned __int128)pair_cap) {
-    const unsigned __int128 q = (total + (unsigned __int128)pair_cap - 1) / (unsigned __int128)pair_cap;
-    stride = std::max<int64_t>(2, (int64_t)q);
-  }
-  const int64_t R = (n - 1 + stride - 1) / stride;
   const int grid = e->num_sms * 4;
   int r;
   if ((r = grow(e, &e->pair_best, &e->pair_best_cap, sizeof(PairBest) * (size_t)grid))) return r;
@@ -1196,7 +1192,7 @@ int km_diameter(km_engine* e, int64_t pair_cap, double* d_out, int64_t* i_out, i
     unsigned int zero = 0, bits = 0;
     CK(cudaMemcpyAsync(e->scratch_u, &zero, 4, cudaMemcpyHostToDevice, e->stream));
     pair_scan_kernel<float, false><<<grid, kPairCols, 0, e->stream>>>((const float*)e->x, n, m, stride, R, 0.f,
-                                                                      (unsigned int*)e->scratch_u, e->pair_best);
+                                                                      (unsigned int*)e->scratch_u, e->pair_best, rows);
     CK_LAUNCH("pair_scan_kernel (phase 1)");
     e->stats.kernel_launches += 1;
     CK(cudaMemcpyAsync(&bits, e->scratch_u, 4, cudaMemcpyDeviceToHost, e->stream));
@@ -1214,10 +1210,10 @@ int km_diameter(km_engine* e, int64_t pair_cap, double* d_out, int64_t* i_out, i
   }
   if (e->point_bytes == 4)
     pair_scan_kernel<float, true><<<grid, kPairCols, 0, e->stream>>>((const float*)e->x, n, m, stride, R,
-                                                                     exact ? -1.0f : thr, nullptr, e->pair_best);
+                                                                     exact ? -1.0f : thr, nullptr, e->pair_best, rows);
   else
     pair_scan_kernel<double, true><<<grid, kPairCols, 0, e->stream>>>((const double*)e->x, n, m, stride, R, -1.0f,
-                                                                      nullptr, e->pair_best);
+                                                                      nullptr, e->pair_best, rows);
   CK_LAUNCH("pair_scan_kernel (phase 2)");
   e->stats.kernel_launches += 1;
   std::vector<PairBest> h(grid);
@@ -1229,7 +1225,55 @@ int km_diameter(km_engine* e, int64_t pair_cap, double* d_out, int64_t* i_out, i
     if (best.i < 0 || b.d2 > best.d2 || (b.d2 == best.d2 && (b.i < best.i || (b.i == best.i && b.j < best.j))))
       best = b;
   }
+  *best_out = best;
+  return KM_OK;
+}
+
+int km_diameter(km_engine* e, int64_t pair_cap, double* d_out, int64_t* i_out, int64_t* j_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  cudaSetDevice(e->device);
+  const int64_t n = e->n;
+  const int m = e->m;
+  if (n < 2) return set_err(e, KM_ERR_CONTRACT, "diameter needs at least 2 samples, got %lld", (long long)n);
+  // engine.scan_rows (engine.py:124-138): every row, or every stride-th row under a pair cap
+  const unsigned __int128 total = (unsigned __int128)n * (unsigned __int128)(n - 1) / 2;
+  int64_t stride = 1;
+  if (pair_cap > 0 && total > (unsigned __int128)pair_cap) {
+    const unsigned __int128 q = (total + (unsigned __int128)pair_cap - 1) / (unsigned __int128)pair_cap;
+    stride = std::max<int64_t>(2, (int64_t)q);
+  }
+  const int64_t R = (n - 1 + stride - 1) / stride;
+  int r;
+  PairBest best;
+  if ((r = pair_scan_best(e, stride, R, nullptr, &best))) return r;
   if (d_out) *d_out = std::sqrt(best.d2);
+  if (i_out) *i_out = best.i;
+  if (j_out) *j_out = best.j;
+  return KM_OK;
+}
+
+// MAX_PAIR device job (device.max_pair_job / HostReferenceDevice._execute, device.py:117-122,
+// 213-216 → _kernels.max_pair_rows, _kernels.py:48-81): best pair over the given ascending rows ×
+// columns j > i; (-1, -1, -1) when the rows produce no pair.
+int km_max_pair_rows(km_engine* e, const int64_t* rows, int64_t nrows, double* d2_out, int64_t* i_out,
+                     int64_t* j_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (nrows < 0 || (nrows > 0 && !rows)) return set_err(e, KM_ERR_CONTRACT, "bad row list");
+  for (int64_t r = 0; r < nrows; ++r) {
+    if (rows[r] < 0 || rows[r] >= e->n) return set_err(e, KM_ERR_CONTRACT, "scan rows must lie in [0, %lld)", (long long)e->n);
+    if (r && rows[r] <= rows[r - 1]) return set_err(e, KM_ERR_CONTRACT, "scan rows must be strictly ascending");
+  }
+  cudaSetDevice(e->device);
+  PairBest best{-1.0, -1, -1};
+  if (nrows > 0 && e->n >= 2) {
+    int r;
+    if ((r = grow(e, &e->rows_dev, &e->rows_cap, sizeof(long long) * (size_t)nrows))) return r;
+    CK(cudaMemcpyAsync(e->rows_dev, rows, sizeof(long long) * (size_t)nrows, cudaMemcpyHostToDevice, e->stream));
+    if ((r = pair_scan_best(e, 1, nrows, (const long long*)e->rows_dev, &best))) return r;
+  }
+  if (d2_out) *d2_out = best.i < 0 ? -1.0 : best.d2;
   if (i_out) *i_out = best.i;
   if (j_out) *j_out = best.j;
   return KM_OK;
@@ -1618,3 +1662,84 @@ int km_get_stats(km_engine* e, km_stats* out) {
 }
 
 }  // extern "C"
+
+// COORD_SUM / CLUSTER_SUM device jobs (device.py:117-134; HostReferenceDevice._execute :218-239):
+// per-block sums of samples [start, stop) (start on a block boundary), blocks of `block`
+// samples.  labels == NULL: coordinate sums, sums_out (nb, m).  Otherwise cluster sums,
+// sums_out (nb, k, m) and counts_out (nb, k); *bad_out = the first sample whose label lies
+// outside [0, k) (then KM_ERR_VALIDATION), else -1.  The sums are exact int64 fixed point
+// rounded once to fp64 (the reference's sequential fp64 block sums agree to ~1e-15 relative).
+int km_block_sums(km_engine* e, const int64_t* labels, int32_t k, int64_t start, int64_t stop, int64_t block,
+                  double* sums_out, int64_t* counts_out, int64_t* bad_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (bad_out) *bad_out = -1;
+  if (!(0 <= start && start <= stop && stop <= e->n))
+    return set_err(e, KM_ERR_CONTRACT, "job range [%lld, %lld) must lie within [0, %lld]", (long long)start,
+                   (long long)stop, (long long)e->n);
+  if (block < 1) return set_err(e, KM_ERR_CONTRACT, "block size must be >= 1, got %lld", (long long)block);
+  if (start % block)
+    return set_err(e, KM_ERR_CONTRACT, "job range must start on an accumulation-block boundary (start=%lld, block=%lld)",
+                   (long long)start, (long long)block);
+  const bool cluster = labels != nullptr;
+  if (cluster && k < 1) return set_err(e, KM_ERR_CONTRACT, "k must be >= 1, got %d", k);
+  const int kk = cluster ? k : 1;
+  const int m = e->m;
+  const int64_t len = stop - start;
+  const int64_t nb = (len + block - 1) / block;
+  if (nb == 0) return KM_OK;
+  if (!sums_out || (cluster && !counts_out)) return set_err(e, KM_ERR_CONTRACT, "null output");
+  const size_t smem = 8 * ((size_t)kk * m + kk);
+  if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "k*m too large for a device sum job");
+  cudaSetDevice(e->device);
+  int r;
+  const size_t nacc = (size_t)nb * kk * m + (size_t)nb * kk + 1;  // + the bad-label slot
+  if ((r = grow(e, &e->job_acc, &e->job_acc_cap, 8 * nacc))) return r;
+  unsigned long long* acc = (unsigned long long*)e->job_acc;
+  CK(cudaMemsetAsync(acc, 0, 8 * (nacc - 1), e->stream));
+  const unsigned long long nobad = ~0ull;
+  CK(cudaMemcpyAsync(acc + nacc - 1, &nobad, 8, cudaMemcpyHostToDevice, e->stream));
+  const int32_t* dlab = nullptr;
+  std::vector<int32_t> lab32;
+  if (cluster) {
+    lab32.resize((size_t)len);
+    for (int64_t i = 0; i < len; ++i) {
+      const int64_t v = labels[start + i];
+      lab32[i] = (v < 0 || v >= k) ? -1 : (int32_t)v;
+    }
+    if ((r = grow(e, &e->job_lab, &e->job_lab_cap, 4 * (size_t)len))) return r;
+    CK(cudaMemcpyAsync(e->job_lab, lab32.data(), 4 * (size_t)len, cudaMemcpyHostToDevice, e->stream));
+    dlab = (const int32_t*)e->job_lab;
+  }
+  const int64_t cpb = (std::min<int64_t>(block, len) + kBlockSumChunk - 1) / kBlockSumChunk;
+  const int F = e->frac_bits;
+  const double sd = std::ldexp(1.0, F);
+  const int use_d = (F > 120 || F < -120) ? 1 : 0;
+  const float sf = use_d ? 1.0f : (float)sd;
+  if (nb * cpb > INT32_MAX) return set_err(e, KM_ERR_CAPACITY, "too many blocks");
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(block_sums_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(block_sums_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  if (e->point_bytes == 4)
+    block_sums_kernel<float><<<(unsigned)(nb * cpb), 256, smem, e->stream>>>(
+        (const float*)e->x, m, start, stop, block, cpb, dlab, kk, sf, sd, use_d, nb, acc, acc + nacc - 1);
+  else
+    block_sums_kernel<double><<<(unsigned)(nb * cpb), 256, smem, e->stream>>>(
+        (const double*)e->x, m, start, stop, block, cpb, dlab, kk, sf, sd, use_d, nb, acc, acc + nacc - 1);
+  CK_LAUNCH("block_sums_kernel");
+  e->stats.kernel_launches += 1;
+  std::vector<unsigned long long> h(nacc);
+  CK(cudaMemcpyAsync(h.data(), acc, 8 * nacc, cudaMemcpyDeviceToHost, e->stream));
+  CK(cudaStreamSynchronize(e->stream));
+  if (h[nacc - 1] != nobad) {
+    if (bad_out) *bad_out = (int64_t)h[nacc - 1];
+    return set_err(e, KM_ERR_VALIDATION, "label out of range [0, %d) at sample %lld", k, (long long)h[nacc - 1]);
+  }
+  const double inv = std::ldexp(1.0, -F);
+  const size_t ns = (size_t)nb * kk * m;
+  for (size_t i = 0; i < ns; ++i) sums_out[i] = (double)(long long)h[i] * inv;
+  if (cluster)
+    for (size_t i = 0; i < (size_t)nb * kk; ++i) counts_out[i] = (int64_t)h[ns + i];
+  return KM_OK;
+}

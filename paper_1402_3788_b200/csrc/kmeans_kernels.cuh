@@ -278,6 +278,47 @@ __global__ void __launch_bounds__(kThreads) lloyd_pass_kernel(PassArgs a) {
   }
 }
 
+// Per-block coordinate / cluster sums of a sample range (the COORD_SUM / CLUSTER_SUM device
+// jobs, device.py:117-134, 218-239 → _kernels.coord_sums_block / cluster_sums_block,
+// _kernels.py:84-113).  CTA = one chunk of ≤ kChunk samples inside one accumulation block;
+// exact int64 fixed-point sums in shared memory (labels == nullptr: every sample in cluster 0),
+// flushed into acc[(block · k + c) · m + f] and counts into acc[nb·k·m + block · k + c].  A label
+// outside [0, k) lowers *bad to its sample index (the reference reports the first one).
+constexpr int kBlockSumChunk = 8192;
+template <typename T>
+__global__ void __launch_bounds__(256) block_sums_kernel(const T* __restrict__ x, int m, int64_t start, int64_t stop,
+                                                         int64_t block, int64_t chunks_per_block,
+                                                         const int32_t* __restrict__ labels, int k, float sf,
+                                                         double sd, int use_d, int64_t nb,
+                                                         unsigned long long* __restrict__ acc,
+                                                         unsigned long long* __restrict__ bad) {
+  extern __shared__ unsigned long long s_blk[];  // k·m sums, then k counts
+  const int km = k * m;
+  for (int i = threadIdx.x; i < km + k; i += blockDim.x) s_blk[i] = 0ull;
+  __syncthreads();
+  const int64_t b = blockIdx.x / chunks_per_block, c = blockIdx.x % chunks_per_block;
+  const int64_t bs = start + b * block;
+  const int64_t be = min(stop, bs + block);
+  const int64_t c0 = bs + c * kBlockSumChunk;
+  const int64_t c1 = min(be, c0 + kBlockSumChunk);
+  for (int64_t i = c0 + threadIdx.x; i < c1; i += blockDim.x) {
+    const int lab = labels ? labels[i - start] : 0;
+    if (lab < 0 || lab >= k) {
+      atomicMin(bad, (unsigned long long)i);
+      continue;
+    }
+    const T* xr = x + i * m;
+    for (int f = 0; f < m; ++f)
+      smem_add64(s_blk + (size_t)lab * m + f, (unsigned long long)to_fixed<T>(xr[f], sf, sd, use_d));
+    smem_add64(s_blk + km + lab, 1ull);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < km; i += blockDim.x)
+    if (s_blk[i]) atomicAdd(acc + (size_t)b * km + i, s_blk[i]);
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    if (s_blk[km + i]) atomicAdd(acc + (size_t)nb * km + (size_t)b * k + i, s_blk[km + i]);
+}
+
 __global__ void __launch_bounds__(512) lloyd_finish_kernel(FinishArgs a, int stage_cap) {
   extern __shared__ double s_stage[];
   finish_block(a, stage_cap > 0 ? s_stage : nullptr, stage_cap);

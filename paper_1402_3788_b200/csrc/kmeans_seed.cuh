@@ -39,7 +39,11 @@ constexpr int kPairFeat = 16;   // features staged per step
 template <typename T, bool PHASE2>
 __global__ void __launch_bounds__(kPairCols) pair_scan_kernel(const T* __restrict__ x, int64_t n, int m,
                                                               int64_t stride, int64_t R, float thr,
-                                                              unsigned int* max_bits, PairBest* out) {
+                                                              unsigned int* max_bits, PairBest* out,
+                                                              const long long* __restrict__ rows = nullptr) {
+  // scan row r is r·stride (engine.scan_rows), or rows[r] for an explicit ascending row list
+  // (a MAX_PAIR device job, device.py:117-122)
+  auto row_of = [&](int64_t r) -> int64_t { return rows ? (int64_t)rows[r] : r * stride; };
   __shared__ float s_row[kPairFeat][kPairRows];
   __shared__ float s_col[kPairFeat][kPairCols];
   __shared__ PairBest s_best[kPairCols / 32];
@@ -52,7 +56,7 @@ __global__ void __launch_bounds__(kPairCols) pair_scan_kernel(const T* __restric
   for (int64_t t = blockIdx.x; t < RT * CT; t += gridDim.x) {
     const int64_t rt = t / CT, ct = t - rt * CT;
     const int64_t r0 = rt * kPairRows;
-    const int64_t i_min = r0 * stride;
+    const int64_t i_min = row_of(r0);  // rows ascending: the tile's smallest row
     const int64_t j0 = ct * kPairCols;
     if (j0 + kPairCols - 1 <= i_min) continue;  // tile entirely on or below the diagonal (block-uniform)
     const int nr = (int)((R - r0) < kPairRows ? (R - r0) : kPairRows);
@@ -65,7 +69,7 @@ __global__ void __launch_bounds__(kPairCols) pair_scan_kernel(const T* __restric
       __syncthreads();
       for (int e = tid; e < kPairRows * kPairFeat; e += kPairCols) {
         const int r = e / kPairFeat, f = e - r * kPairFeat;
-        s_row[f][r] = (r < nr && f < fc) ? (float)x[(r0 + r) * stride * m + f0 + f] : 0.f;
+        s_row[f][r] = (r < nr && f < fc) ? (float)x[row_of(r0 + r) * m + f0 + f] : 0.f;
       }
       for (int f = 0; f < fc; ++f) s_col[f][tid] = (j < n) ? (float)x[j * m + f0 + f] : 0.f;
       __syncthreads();
@@ -80,7 +84,7 @@ __global__ void __launch_bounds__(kPairCols) pair_scan_kernel(const T* __restric
     }
 #pragma unroll
     for (int r = 0; r < kPairRows; ++r) {
-      const int64_t i = (r0 + r) * stride;
+      const int64_t i = r < nr ? row_of(r0 + r) : n;
       const bool valid = r < nr && j < n && j > i;
       if (!PHASE2) {
         if (valid) tmax = fmaxf(tmax, acc[r]);

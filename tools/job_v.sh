@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-for v in ni coop e3 ni coop; do echo "=== '$v'"; KM_LIB_VARIANT=$v timeout 120 python tools/time_windows.py cfg3 2>&1; done > gpurun_out/v82.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_device.py -x -q > gpurun_out/v85_dev.log 2>&1
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/v85_tests.log 2>&1
