@@ -197,8 +197,10 @@ KM_API int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, 
 KM_API int km_get_stats(km_engine* e, km_stats* out);
 KM_API int km_reset_stats(km_engine* e);
 /* Kernel path for the fused pass: 0 = auto (tcgen05 tensor-core pass when the
- * shape allows: fp32 points, m ≤ 31, k ≤ 64; SIMT otherwise), 1 = SIMT only,
- * 2 = tensor core required (error if not available). */
+ * shape allows: fp32 points, m ≤ 31, k ≤ 128; SIMT otherwise — register-blocked
+ * for fp32 points with m ≤ 32, k ≥ 32), 1 = SIMT only, 2 = tensor core required
+ * (error if not available), 3 = SIMT one point per thread (no register blocking;
+ * a test hook for the blocked kernel). */
 KM_API int km_set_kernel_path(km_engine* e, int32_t path);
 KM_API int km_kernel_path(km_engine* e, int32_t* out);   /* path the next pass uses: 1 SIMT, 2 tensor core */
 /* Test hook: raw tensor-core filter scores S~[n×k] = ‖c~‖² − 2x·c~ (fp32) for the given centres. */

@@ -94,7 +94,7 @@ struct km_engine {
   unsigned long long* dlt = nullptr;     // resident loop: [3][k·m + k] per-pass deltas
   bool resident_unfit = false;           // the resident TC loop does not fit this shape (use per-iteration launches)
   bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
-  int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required
+  int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required, 3 SIMT without register blocking
   float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
 
   km_stats stats{};
@@ -219,13 +219,52 @@ static int launch_pass_mp(km_engine* e, const PassArgs& a, size_t smem) {
 }
 
 enum PassMode { PASS_ASSIGN_SUMS = 0, PASS_ASSIGN_ONLY = 1, PASS_SUMS_ONLY = 2 };
+// register-blocked large-K pass (fp32 points, m ≤ 32, k ≥ kBlockedMinK): MP = the register row
+static int blk_mp_for(int m) { return m <= 8 ? 8 : m <= 16 ? 16 : m <= 24 ? 24 : m == 25 ? 25 : m <= 28 ? 28 : m <= 32 ? 32 : 0; }
+constexpr int kBlockedMinK = 32;
+static size_t blocked_smem_bytes(const km_engine* e, int mp, bool smem_acc) {
+  const size_t kp8 = ((size_t)e->k + 7) & ~size_t(7);
+  return (size_t)mp * kp8 * 4 + kp8 * 4 + (smem_acc ? ((size_t)e->k * e->m + e->k) * 8 : 0);
+}
+
+template <int MP, bool S, bool SA>
+static int launch_blocked_t(km_engine* e, const PassArgs& a, size_t smem) {
+  auto kern = lloyd_pass_blocked_kernel<MP, S, SA>;
+  if (smem > 48 * 1024) {
+    cudaError_t c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (c != cudaSuccess) return cuda_fail(e, c, "cudaFuncSetAttribute(blocked pass smem)");
+  }
+  int per_sm = 0;
+  cudaError_t c = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kBlkThreads, smem);
+  if (c != cudaSuccess) return cuda_fail(e, c, "occupancy");
+  if (per_sm < 1) return set_err(e, KM_ERR_CAPACITY, "blocked pass kernel does not fit on an SM (smem %zu B)", smem);
+  const int64_t ntiles = (a.n + kBlkTileRows - 1) / kBlkTileRows;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)per_sm * e->num_sms));
+  kern<<<(unsigned)grid, kBlkThreads, smem, e->stream>>>(a, (e->k + 7) & ~7);
+  CK_LAUNCH("lloyd_pass_blocked_kernel launch");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
+template <bool S, bool SA>
+static int launch_blocked_mp(km_engine* e, const PassArgs& a, size_t smem, int mp) {
+  switch (mp) {
+    case 8: return launch_blocked_t<8, S, SA>(e, a, smem);
+    case 16: return launch_blocked_t<16, S, SA>(e, a, smem);
+    case 24: return launch_blocked_t<24, S, SA>(e, a, smem);
+    case 25: return launch_blocked_t<25, S, SA>(e, a, smem);
+    case 28: return launch_blocked_t<28, S, SA>(e, a, smem);
+    default: return launch_blocked_t<32, S, SA>(e, a, smem);
+  }
+}
+
 
 // tensor-core path: fp32 resident points, m ≤ 31 ([xh|xl] + the ones column fit one 128-byte
 // fp16 row), k ≤ 128 (N = 2·KP ≤ 256 per MMA; 2 warpgroups × 2·KP TMEM columns ≤ 512)
 static bool tc_eligible(const km_engine* e) {
   return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= 128;
 }
-static bool use_tc(const km_engine* e) { return e->path_pref != 1 && tc_eligible(e); }
+static bool use_tc(const km_engine* e) { return e->path_pref != 1 && e->path_pref != 3 && tc_eligible(e); }
 
 static int tc_mp_for(int m) { return m <= 7 ? 7 : m <= 15 ? 15 : m <= 23 ? 23 : 31; }
 
@@ -411,6 +450,16 @@ static int launch_pass(km_engine* e, PassMode mode, bool gated, bool fuse_finish
   if (smem > e->smem_optin)
     return set_err(e, KM_ERR_CAPACITY, "k=%d, m=%d needs %zu B of shared memory per CTA (max %zu)", e->k, e->m, smem,
                    e->smem_optin);
+  if (eb == 4 && A && e->k >= kBlockedMinK && blk_mp_for(e->m) > 0 && e->path_pref != 3) {
+    const int mp = blk_mp_for(e->m);
+    const size_t bs_sa = blocked_smem_bytes(e, mp, true), bs_g = blocked_smem_bytes(e, mp, false);
+    if (bs_g <= e->smem_optin) {
+      const bool bsa = bs_sa <= e->smem_optin;
+      const size_t bsm = bsa ? bs_sa : bs_g;
+      if (mode == PASS_ASSIGN_SUMS) return bsa ? launch_blocked_mp<true, true>(e, a2, bsm, mp) : launch_blocked_mp<true, false>(e, a2, bsm, mp);
+      return bsa ? launch_blocked_mp<false, true>(e, a2, bsm, mp) : launch_blocked_mp<false, false>(e, a2, bsm, mp);
+    }
+  }
   if (eb == 4) {
     if (mode == PASS_ASSIGN_SUMS) return sa ? launch_pass_mp<float, true, true, true>(e, a2, smem) : launch_pass_mp<float, true, true, false>(e, a2, smem);
     if (mode == PASS_ASSIGN_ONLY) return sa ? launch_pass_mp<float, true, false, true>(e, a2, smem) : launch_pass_mp<float, true, false, false>(e, a2, smem);
@@ -1600,7 +1649,8 @@ int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, int64_t
 
 int km_set_kernel_path(km_engine* e, int32_t path) {
   if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
-  if (path < 0 || path > 2) return set_err(e, KM_ERR_CONTRACT, "path must be 0 (auto), 1 (SIMT) or 2 (tensor core)");
+  if (path < 0 || path > 3)
+    return set_err(e, KM_ERR_CONTRACT, "path must be 0 (auto), 1 (SIMT), 2 (tensor core) or 3 (SIMT, one point per thread)");
   e->path_pref = path;
   return KM_OK;
 }

@@ -278,6 +278,200 @@ __global__ void __launch_bounds__(kThreads) lloyd_pass_kernel(PassArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register-blocked fused pass for large K (fp32 points, m ≤ MP ≤ 32): the FP32-bound regime
+// (BASELINE cfg4, K = 512).  Each thread owns kBlkPts points (coordinates in registers) and walks
+// the centres in chunks of kBlkC: per feature f, kBlkC/4 broadcast LDS.128 of the transposed
+// operand wt[f][c] feed kBlkPts·kBlkC independent FMAs (an SGEMM-style outer product), against
+// 1 LDS.128 per 4 FMAs in lloyd_pass_kernel.  Every score is the same FMA chain as score_reg
+// (a = ‖c‖², then a = fma(x_f, −2c_f, a) for f ascending), so the filter, its certificate and the
+// exact fp64 recheck (same candidates, same lowest-index rule) decide bit-identical labels.
+// The FMAs are packed fp32x2 (FFMA2, one issue slot for both points' lanes).
+// Sums: the per-CTA fixed-point accumulators of lloyd_pass_kernel.
+// ---------------------------------------------------------------------------
+constexpr int kBlkThreads = 384;
+constexpr int kBlkPts = 2;
+constexpr int kBlkC = 8;
+constexpr int kBlkTileRows = kBlkThreads * kBlkPts;
+
+static_assert(kBlkPts == 2, "the blocked pass pairs its two points in fp32x2 registers");
+__device__ __forceinline__ unsigned long long pack_f32x2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void unpack_f32x2(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ float lane_f32x2(unsigned long long v, int p) {
+  float lo, hi;
+  unpack_f32x2(v, lo, hi);
+  return p ? hi : lo;
+}
+// lane-wise fma.rn (no ftz): FFMA2 on sm_100a
+__device__ __forceinline__ unsigned long long ffma_f32x2(unsigned long long a, unsigned long long b,
+                                                         unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
+__device__ __forceinline__ void blk_take(float s, int c, float& best, float& min2, int& bi) {
+  min2 = fminf(min2, fmaxf(best, s));  // = (s < best ? best : min(min2, s)), best ≤ min2
+  const bool lt = s < best;
+  bi = lt ? c : bi;
+  best = lt ? s : best;
+}
+
+template <int MP, bool DO_SUMS, bool SMEM_ACC>
+__global__ void __launch_bounds__(kBlkThreads, 1) lloyd_pass_blocked_kernel(PassArgs a, int kp8) {
+  if (a.gate && (a.st->done || a.st->need_host)) return;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int m = a.m, k = a.k, tid = threadIdx.x;
+  // layout: [wt MP × kp8 f32][cn kp8 f32][acc k·m u64][cnt k u64]
+  float* s_wt = reinterpret_cast<float*>(smem);
+  float* s_cn = s_wt + (size_t)MP * kp8;
+  unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(s_cn + kp8);  // kp8·4 B keeps 16 B alignment
+  unsigned long long* s_cnt = s_acc + (size_t)k * m;
+  for (int i = tid; i < MP * kp8; i += kBlkThreads) {
+    const int f = i / kp8, c = i - f * kp8;
+    s_wt[i] = (c < k && f < m) ? a.w[(size_t)c * a.mpad + f] : 0.f;
+  }
+  for (int c = tid; c < kp8; c += kBlkThreads) s_cn[c] = c < k ? a.cn[c] : __int_as_float(0x7f800000);
+  if (SMEM_ACC)
+    for (int i = tid; i < k * m + k; i += kBlkThreads) s_acc[i] = 0ull;
+  __syncthreads();
+  unsigned long long* g_acc = a.part;
+  unsigned long long* g_cnt = a.part + (size_t)k * m;
+  unsigned long long* acc = SMEM_ACC ? s_acc : g_acc;
+  unsigned long long* cnt = SMEM_ACC ? s_cnt : g_cnt;
+  const float cmax = a.cmax[0];
+  const float* __restrict__ X = reinterpret_cast<const float*>(a.x);
+  const int64_t ntiles = (a.n + kBlkTileRows - 1) / kBlkTileRows;
+  unsigned int my_rechecks = 0;
+
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // the two points of a thread share one packed fp32x2 FMA per (feature, centre): FFMA2 with the
+    // centre operand broadcast; each lane is the IEEE fma.rn of score_reg (bit-identical chains)
+    unsigned long long xp2[MP];
+    int64_t row[kBlkPts];
+    bool live[kBlkPts];
+#pragma unroll
+    for (int p = 0; p < kBlkPts; ++p) {
+      row[p] = tile * kBlkTileRows + p * kBlkThreads + tid;
+      live[p] = row[p] < a.n;
+    }
+    {
+      const float* x0 = X + (live[0] ? row[0] : 0) * m;
+      const float* x1 = X + (live[1] ? row[1] : 0) * m;
+#pragma unroll
+      for (int f = 0; f < MP; ++f)
+        xp2[f] = pack_f32x2((live[0] && f < m) ? __ldg(x0 + f) : 0.f, (live[1] && f < m) ? __ldg(x1 + f) : 0.f);
+    }
+    float best[kBlkPts], min2[kBlkPts];
+    int bi[kBlkPts];
+#pragma unroll
+    for (int p = 0; p < kBlkPts; ++p) best[p] = min2[p] = __int_as_float(0x7f800000), bi[p] = 0;
+    for (int c0 = 0; c0 < kp8; c0 += kBlkC) {
+      unsigned long long s2[kBlkC];
+      const float4 n0 = *reinterpret_cast<const float4*>(s_cn + c0);
+      const float4 n1 = *reinterpret_cast<const float4*>(s_cn + c0 + 4);
+      s2[0] = pack_f32x2(n0.x, n0.x), s2[1] = pack_f32x2(n0.y, n0.y);
+      s2[2] = pack_f32x2(n0.z, n0.z), s2[3] = pack_f32x2(n0.w, n0.w);
+      s2[4] = pack_f32x2(n1.x, n1.x), s2[5] = pack_f32x2(n1.y, n1.y);
+      s2[6] = pack_f32x2(n1.z, n1.z), s2[7] = pack_f32x2(n1.w, n1.w);
+#pragma unroll
+      for (int f = 0; f < MP; ++f) {
+        const float4 w0 = *reinterpret_cast<const float4*>(s_wt + (size_t)f * kp8 + c0);
+        const float4 w1 = *reinterpret_cast<const float4*>(s_wt + (size_t)f * kp8 + c0 + 4);
+        s2[0] = ffma_f32x2(xp2[f], pack_f32x2(w0.x, w0.x), s2[0]);
+        s2[1] = ffma_f32x2(xp2[f], pack_f32x2(w0.y, w0.y), s2[1]);
+        s2[2] = ffma_f32x2(xp2[f], pack_f32x2(w0.z, w0.z), s2[2]);
+        s2[3] = ffma_f32x2(xp2[f], pack_f32x2(w0.w, w0.w), s2[3]);
+        s2[4] = ffma_f32x2(xp2[f], pack_f32x2(w1.x, w1.x), s2[4]);
+        s2[5] = ffma_f32x2(xp2[f], pack_f32x2(w1.y, w1.y), s2[5]);
+        s2[6] = ffma_f32x2(xp2[f], pack_f32x2(w1.z, w1.z), s2[6]);
+        s2[7] = ffma_f32x2(xp2[f], pack_f32x2(w1.w, w1.w), s2[7]);
+      }
+#pragma unroll
+      for (int j = 0; j < kBlkC; ++j) {
+        float lo, hi;
+        unpack_f32x2(s2[j], lo, hi);
+        blk_take(lo, c0 + j, best[0], min2[0], bi[0]);
+        blk_take(hi, c0 + j, best[1], min2[1], bi[1]);
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < kBlkPts; ++p) {
+      if (!live[p]) continue;
+      float nx2 = 0.f;
+#pragma unroll
+      for (int f = 0; f < MP; ++f) nx2 = __fmaf_rn(lane_f32x2(xp2[f], p), lane_f32x2(xp2[f], p), nx2);
+      const float t = __fmaf_rn(sqrtf(nx2), a.nx_inflate, cmax);
+      const float E = __fmaf_rn(a.err_coef * t, t, a.err_floor);
+      const float thr = best[p] + 2.f * E;
+      int lab = bi[p];
+      if (a.exact_only || !(min2[p] > thr)) {
+        // exact recheck (rare, divergent): every centre whose filter score is within 2E of the best
+        ++my_rechecks;
+        double bd = 0.0;
+        int bl = -1;
+        for (int c = 0; c < k; ++c) {
+          bool cand = a.exact_only != 0;
+          if (!cand) {
+            float sc = s_cn[c];
+#pragma unroll
+            for (int f = 0; f < MP; ++f) sc = __fmaf_rn(lane_f32x2(xp2[f], p), s_wt[(size_t)f * kp8 + c], sc);
+            cand = sc <= thr;
+          }
+          if (cand) {
+            const double* cc = a.c64 + (size_t)c * m;
+            double d2 = 0.0;
+#pragma unroll
+            for (int f = 0; f < MP; ++f) {
+              if (f < m) {
+                const double d = __dsub_rn((double)lane_f32x2(xp2[f], p), cc[f]);
+                d2 = __dadd_rn(d2, __dmul_rn(d, d));
+              }
+            }
+            if (bl < 0 || d2 < bd) { bd = d2; bl = c; }
+          }
+        }
+        lab = bl;
+      }
+      a.labels[row[p]] = lab;
+      if (SMEM_ACC) {
+        atomicAdd(reinterpret_cast<unsigned int*>(cnt + lab), 1u);  // counts < 2^32 per CTA
+        if (DO_SUMS) {
+          unsigned long long* dst = acc + (size_t)lab * m;
+#pragma unroll
+          for (int f = 0; f < MP; ++f)
+            if (f < m) smem_add64(dst + f, (unsigned long long)to_fixed<float>(lane_f32x2(xp2[f], p), a.scale_f, a.scale_d, a.use_dscale));
+        }
+      } else {
+        atomicAdd(cnt + lab, 1ull);
+        if (DO_SUMS) {
+          unsigned long long* dst = acc + (size_t)lab * m;
+#pragma unroll
+          for (int f = 0; f < MP; ++f)
+            if (f < m) atomicAdd(dst + f, (unsigned long long)to_fixed<float>(lane_f32x2(xp2[f], p), a.scale_f, a.scale_d, a.use_dscale));
+        }
+      }
+    }
+  }
+  unsigned int wsum = my_rechecks;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(0xffffffffu, wsum, o);
+  if ((tid & 31) == 0 && wsum) atomicAdd(&a.st->rechecked, (unsigned long long)wsum);
+  if (SMEM_ACC) {
+    __syncthreads();
+    for (int i = tid; i < k * m; i += kBlkThreads)
+      if (s_acc[i]) atomicAdd(g_acc + i, s_acc[i]);
+    for (int i = tid; i < k; i += kBlkThreads)
+      if (s_cnt[i]) atomicAdd(g_cnt + i, s_cnt[i]);
+  }
+}
+
 // Per-block coordinate / cluster sums of a sample range (the COORD_SUM / CLUSTER_SUM device
 // jobs, device.py:117-134, 218-239 → _kernels.coord_sums_block / cluster_sums_block,
 // _kernels.py:84-113).  CTA = one chunk of ≤ kChunk samples inside one accumulation block;

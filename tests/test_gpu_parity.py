@@ -232,3 +232,37 @@ def test_full_size_properties(native, n, m, k, iters):
     for c in np.flatnonzero(~occ):  # repaired: centre = the relabelled sample
         assert np.array_equal(c_next[c], xd[np.flatnonzero(lab == c)[0]])
     eng.close()
+
+
+# --- register-blocked large-K SIMT pass (lloyd_pass_blocked_kernel) ------------------------------
+
+
+def run_path(native, x, c0, iters, path):
+    eng = native.NativeEngine(0)
+    eng.load(x)
+    eng.set_kernel_path(path)
+    centers, counts, labels, it, conv = eng.lloyd(c0, iters, 0.0)
+    st = eng.stats()
+    eng.close()
+    return dict(centers=centers, counts=counts, labels=labels, iterations=it, converged=conv, stats=st)
+
+
+@pytest.mark.parametrize("n,m,k,iters", [(20_000, 7, 33, 20), (30_000, 16, 200, 6), (25_000, 25, 512, 4),
+                                         (9_999, 32, 100, 10), (12_000, 26, 40, 12), (15_000, 25, 1000, 3),
+                                         (1_025, 25, 300, 5)])
+def test_blocked_pass_vs_oracle_and_unblocked(native, n, m, k, iters):
+    """Large-K SIMT pass (fp32, k ≥ 32, m ≤ 32; k = 1000 exceeds the shared-memory accumulators and
+    takes the global-atomics variant; n = 1025 leaves a ragged last tile): labels, counts and
+    centres equal the C oracle and are bit-identical to the one-point-per-thread kernel (path 3)."""
+    from oracle import oracle
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(n, m, min(k, n // 2), seed=k + m, dtype=np.float32)
+    c0 = x[:k].astype(np.float64)
+    blk = run_path(native, x, c0, iters, 1)
+    ref = run_path(native, x, c0, iters, 3)
+    want = oracle.lloyd(x.astype(np.float64), c0, max_iters=iters, n_workers=8)
+    check(want, blk, f"blocked {n}x{m}x{k}")
+    assert np.array_equal(blk["labels"], ref["labels"])
+    assert np.array_equal(blk["centers"], ref["centers"])
+    assert np.array_equal(blk["counts"], ref["counts"])
