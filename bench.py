@@ -307,11 +307,28 @@ def run_ours(args, cfg_name):
     # step path has no per-pass events, so its roofline uses the whole step (pass + allreduce + finish)
     pass_ms = st["pass_ms_total"] / st["pass_timed"] if st["pass_timed"] else ms_per_step
     alg_bytes = n * (4 * m + 4)  # points read once (fp32) + int32 labels written once
-    achieved = alg_bytes / (pass_ms * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic_from_profiles(cfg_name), "kernel": "lloyd_pass_tc_kernel (resident loop; per-pass time = launch time / passes)",
-                "kernel_ms_per_pass": pass_ms, "alg_bytes_per_pass": alg_bytes, "peak_kind": peak_kind,
-                "pass_share_of_step": pass_ms / ms_per_step}
+    if k > 128:
+        # compute-bound large-K regime: algorithmic 3·n·K·M flops per pass against the
+        # FP32 pipe peak SMs × 128 lanes × 2 flops × the max SM clock
+        props = torch.cuda.get_device_properties(local)
+        f_max = (clocks or {}).get("sm_max_mhz") or 1965.0
+        fp32_peak = props.multi_processor_count * 256 * f_max * 1e6 / 1e12
+        alg_flops = 3.0 * n * k * m
+        achieved = alg_flops / (pass_ms * 1e-3) / 1e12
+        roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak, "traffic": None,
+                    "kernel": "lloyd_pass_blocked_kernel (register-blocked FFMA2 SIMT pass)",
+                    "kernel_ms_per_pass": pass_ms, "alg_flops_per_pass": alg_flops,
+                    "peak_kind": f"FP32 pipe: {props.multi_processor_count} SMs x 128 lanes x 2 flops x {f_max:.0f} MHz",
+                    "pass_share_of_step": pass_ms / ms_per_step,
+                    "note": "expanded-form filter: M FMAs per (point, centre) = 2nKM flops executed; "
+                            "3nKM is the reference recurrence's algorithmic count"}
+    else:
+        achieved = alg_bytes / (pass_ms * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic_from_profiles(cfg_name), "kernel": "lloyd_pass_tc_kernel (resident loop; per-pass time = launch time / passes)",
+                    "kernel_ms_per_pass": pass_ms, "alg_bytes_per_pass": alg_bytes, "peak_kind": peak_kind,
+                    "pass_share_of_step": pass_ms / ms_per_step}
 
     # e2e: the public API from pinned host buffers, full fit to convergence
     e2e = None
