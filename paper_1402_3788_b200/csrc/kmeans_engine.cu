@@ -734,11 +734,11 @@ static int repair_local(km_engine* e) {
     argmax_partial_kernel<<<e->n_partials, 256, 0, e->stream>>>(e->d2, e->n, e->partials);
     CK_LAUNCH("argmax_partial_kernel");
     if (e->point_bytes == 4)
-      repair_apply_kernel<float><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const float*)e->x, e->k,
+      repair_apply_kernel<float><<<1, 512, 0, e->stream>>>(e->partials, e->n_partials, c, (const float*)e->x, e->k,
                                                           e->m, e->labels, e->d2, e->model_counts, e->cur, e->tot,
                                                           std::ldexp(1.0, e->frac_bits), e->winner);
     else
-      repair_apply_kernel<double><<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, c, (const double*)e->x,
+      repair_apply_kernel<double><<<1, 512, 0, e->stream>>>(e->partials, e->n_partials, c, (const double*)e->x,
                                                            e->k, e->m, e->labels, e->d2, e->model_counts, e->cur,
                                                            e->tot, std::ldexp(1.0, e->frac_bits), e->winner);
     CK_LAUNCH("repair_apply_kernel");
@@ -1514,7 +1514,7 @@ int km_step_repair_candidate(km_engine* e, double* d2_out, int64_t* row_out, dou
   cudaSetDevice(e->device);
   argmax_partial_kernel<<<e->n_partials, 256, 0, e->stream>>>(e->d2, e->n, e->partials);
   CK_LAUNCH("argmax_partial_kernel");
-  argmax_final_kernel<<<1, 32, 0, e->stream>>>(e->partials, e->n_partials, e->winner);
+  argmax_final_kernel<<<1, 512, 0, e->stream>>>(e->partials, e->n_partials, e->winner);
   CK_LAUNCH("argmax_final_kernel");
   ArgMax h{};
   CK(cudaMemcpyAsync(&h, e->winner, sizeof h, cudaMemcpyDeviceToHost, e->stream));

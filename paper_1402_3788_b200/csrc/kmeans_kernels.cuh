@@ -403,26 +403,39 @@ __global__ void __launch_bounds__(kBlkThreads, 1) lloyd_pass_blocked_kernel(Pass
     }
 #pragma unroll
     for (int p = 0; p < kBlkPts; ++p) {
-      if (!live[p]) continue;
-      float nx2 = 0.f;
-#pragma unroll
-      for (int f = 0; f < MP; ++f) nx2 = __fmaf_rn(lane_f32x2(xp2[f], p), lane_f32x2(xp2[f], p), nx2);
-      const float t = __fmaf_rn(sqrtf(nx2), a.nx_inflate, cmax);
-      const float E = __fmaf_rn(a.err_coef * t, t, a.err_floor);
-      const float thr = best[p] + 2.f * E;
+      float thr = 0.f;
+      bool need = false;
       int lab = bi[p];
-      if (a.exact_only || !(min2[p] > thr)) {
-        // exact recheck (rare, divergent): every centre whose filter score is within 2E of the best
-        ++my_rechecks;
+      if (live[p]) {
+        float nx2 = 0.f;
+#pragma unroll
+        for (int f = 0; f < MP; ++f) nx2 = __fmaf_rn(lane_f32x2(xp2[f], p), lane_f32x2(xp2[f], p), nx2);
+        const float t = __fmaf_rn(sqrtf(nx2), a.nx_inflate, cmax);
+        const float E = __fmaf_rn(a.err_coef * t, t, a.err_floor);
+        thr = best[p] + 2.f * E;
+        need = a.exact_only || !(min2[p] > thr);
+      }
+      // exact recheck, warp-cooperative: for each lane whose certificate failed, the 32 lanes split
+      // the centres (c ≡ lane mod 32, ascending), keep the candidates within 2E of the best filter
+      // score, evaluate the reference fp64 recurrence and reduce (d², c) lexicographically — the
+      // lowest index among equal distances, as the serial loop's strict '<' over ascending c
+      unsigned pend = __ballot_sync(0xffffffffu, need);
+      while (pend) {
+        const int src = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const float tthr = __shfl_sync(0xffffffffu, thr, src);
+        float xs[MP];
+#pragma unroll
+        for (int f = 0; f < MP; ++f) xs[f] = __shfl_sync(0xffffffffu, lane_f32x2(xp2[f], p), src);
         double bd = 0.0;
-        int bl = -1;
-        for (int c = 0; c < k; ++c) {
+        int bl = 0x7fffffff;
+        for (int c = (int)(threadIdx.x & 31); c < k; c += 32) {
           bool cand = a.exact_only != 0;
           if (!cand) {
             float sc = s_cn[c];
 #pragma unroll
-            for (int f = 0; f < MP; ++f) sc = __fmaf_rn(lane_f32x2(xp2[f], p), s_wt[(size_t)f * kp8 + c], sc);
-            cand = sc <= thr;
+            for (int f = 0; f < MP; ++f) sc = __fmaf_rn(xs[f], s_wt[(size_t)f * kp8 + c], sc);
+            cand = sc <= tthr;
           }
           if (cand) {
             const double* cc = a.c64 + (size_t)c * m;
@@ -430,15 +443,25 @@ __global__ void __launch_bounds__(kBlkThreads, 1) lloyd_pass_blocked_kernel(Pass
 #pragma unroll
             for (int f = 0; f < MP; ++f) {
               if (f < m) {
-                const double d = __dsub_rn((double)lane_f32x2(xp2[f], p), cc[f]);
+                const double d = __dsub_rn((double)xs[f], cc[f]);
                 d2 = __dadd_rn(d2, __dmul_rn(d, d));
               }
             }
-            if (bl < 0 || d2 < bd) { bd = d2; bl = c; }
+            if (bl == 0x7fffffff || d2 < bd) { bd = d2; bl = c; }
           }
         }
-        lab = bl;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double obd = __shfl_xor_sync(0xffffffffu, bd, o);
+          const int obl = __shfl_xor_sync(0xffffffffu, bl, o);
+          if (obl != 0x7fffffff && (bl == 0x7fffffff || obd < bd || (obd == bd && obl < bl))) { bd = obd; bl = obl; }
+        }
+        if ((int)(threadIdx.x & 31) == src) {
+          lab = bl;
+          ++my_rechecks;
+        }
       }
+      if (!live[p]) continue;
       a.labels[row[p]] = lab;
       if (SMEM_ACC) {
         atomicAdd(reinterpret_cast<unsigned int*>(cnt + lab), 1u);  // counts < 2^32 per CTA
@@ -671,6 +694,36 @@ __device__ __forceinline__ ArgMax argmax_better(ArgMax a, ArgMax b) {
   return a;
 }
 
+// Block-wide reduction of the per-block partials (any blockDim ≤ 1024, multiple of 32):
+// argmax_better is a total order (value desc, index asc), so the result is order-independent.
+// The serial one-thread loop over thousands of partials cost ~100 µs per repair.
+__device__ __forceinline__ ArgMax argmax_reduce_block(const ArgMax* partial, int nparts) {
+  __shared__ ArgMax s_red[32];
+  ArgMax best{-1.0, 0x7fffffffffffffffLL};
+  for (int i = threadIdx.x; i < nparts; i += blockDim.x) best = argmax_better(best, partial[i]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax other;
+    other.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+    other.i = __shfl_xor_sync(0xffffffffu, best.i, o);
+    best = argmax_better(best, other);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (lane == 0) s_red[warp] = best;
+  __syncthreads();
+  if (warp == 0) {
+    best = lane < nw ? s_red[lane] : ArgMax{-1.0, 0x7fffffffffffffffLL};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      ArgMax other;
+      other.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+      other.i = __shfl_xor_sync(0xffffffffu, best.i, o);
+      best = argmax_better(best, other);
+    }
+  }
+  return best;  // valid in thread 0
+}
+
 __global__ void argmax_partial_kernel(const double* __restrict__ d2, int64_t n, ArgMax* partial) {
   ArgMax best{-1.0, (long long)n};
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -705,9 +758,8 @@ template <typename T>
 __global__ void repair_apply_kernel(const ArgMax* partial, int nparts, int c, const T* __restrict__ x, int k, int m,
                                     int32_t* labels, double* d2, long long* model_counts, double* cur,
                                     unsigned long long* tot, double scale_d, ArgMax* winner_out) {
+  const ArgMax best = argmax_reduce_block(partial, nparts);
   if (threadIdx.x != 0) return;
-  ArgMax best = partial[0];
-  for (int i = 1; i < nparts; ++i) best = argmax_better(best, partial[i]);
   const long long s = best.i;
   const int donor = labels[s];
   labels[s] = c;
@@ -721,10 +773,8 @@ __global__ void repair_apply_kernel(const ArgMax* partial, int nparts, int c, co
 
 // Local candidate only (multi-GPU repair: the caller picks the global winner).
 __global__ void argmax_final_kernel(const ArgMax* partial, int nparts, ArgMax* out) {
-  if (threadIdx.x != 0) return;
-  ArgMax best = partial[0];
-  for (int i = 1; i < nparts; ++i) best = argmax_better(best, partial[i]);
-  *out = best;
+  const ArgMax best = argmax_reduce_block(partial, nparts);
+  if (threadIdx.x == 0) *out = best;
 }
 
 // Apply a repair decided across shards.
