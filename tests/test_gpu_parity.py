@@ -266,3 +266,26 @@ def test_blocked_pass_vs_oracle_and_unblocked(native, n, m, k, iters):
     assert np.array_equal(blk["labels"], ref["labels"])
     assert np.array_equal(blk["centers"], ref["centers"])
     assert np.array_equal(blk["counts"], ref["counts"])
+
+
+def test_blocked_pass_ties_and_exact_only(native):
+    """Blocked pass edge cases: duplicated centres and points equidistant from several centres (every
+    such point fails the certificate; the warp-cooperative recheck must return the lowest index, as
+    the reference's strict '<'), and magnitudes past the filter's certified range (exact_only: every
+    centre re-evaluated in fp64)."""
+    from oracle import oracle
+
+    rng = np.random.default_rng(11)
+    grid = rng.integers(-4, 5, size=(6000, 6)).astype(np.float32)  # many exact ties on the lattice
+    c0 = grid[:48].astype(np.float64).copy()
+    c0[10:20] = c0[0:10]  # duplicated centres
+    want = oracle.lloyd(grid.astype(np.float64), c0, max_iters=8)
+    got = run_path(native, grid, c0, 8, 1)
+    check(want, got, "lattice ties")
+    assert got["stats"]["rechecked"] > 0
+    big = (rng.standard_normal((3000, 9)) * 1e20).astype(np.float32)
+    c1 = big[:40].astype(np.float64)
+    want = oracle.lloyd(big.astype(np.float64), c1, max_iters=6)
+    got = run_path(native, big, c1, 6, 1)
+    assert got["iterations"] == want["iterations"] and np.array_equal(got["labels"], want["labels"])
+    assert rel_err(got["centers"] / 1e20, want["centers"] / 1e20) <= 1e-9
