@@ -52,6 +52,9 @@ CONFIGS = {
     "cfg2": (100_000, 10, 8, "n=100,000 M=10 K=8 (single/multi regime boundary)"),
     "cfg3": (2_000_000, 25, 16, "n=2,000,000 M=25 K=16 fp32 blobs (paper headline shape), 1 B200"),
     "cfg4": (2_000_000, 25, 512, "n=2,000,000 M=25 K=512 (compute-bound large-K assignment)"),
+    # the row-sharded config: 64M points on one GPU at N=1 (6.4 GB resident); under torchrun each rank
+    # holds its own n-row shard (weak scaling, as the other configs)
+    "cfg5": (64_000_000, 25, 64, "n=64,000,000 M=25 K=64 (row-shard config), one shard per GPU"),
 }
 METRIC = "Lloyd iters/sec & points·iters/sec at n=2M,M=25,K=16; HBM GB/s vs peak"
 UNIT = "points*iters/s"
