@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(kBlkThreads, 1) lloyd_pass_blocked_kernel(Pass
     int bi[kBlkPts];
 #pragma unroll
     for (int p = 0; p < kBlkPts; ++p) best[p] = min2[p] = __int_as_float(0x7f800000), bi[p] = 0;
+#pragma unroll 2
     for (int c0 = 0; c0 < kp8; c0 += kBlkC) {
       unsigned long long s2[kBlkC];
       const float4 n0 = *reinterpret_cast<const float4*>(s_cn + c0);
