@@ -245,9 +245,77 @@ def seeding():
     print(f"seeding: {len(cases)} cases ({sum(bool(d['degenerate']) for d in cases.values())} degenerate)")
 
 
+def run_iterate_parallel(coords, c0, max_iters=1000, tol=0.0, workers=8):
+    """engine.iterate with the run_multi closures (partition.assign_parallel / update_parallel,
+    partition.py:215-261, 264-305) — bit-identical to run_single for any worker count
+    (the reference's own cross-regime tests), and 8x faster at the benchmark sizes."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from kmeans_regimes.partition import assign_parallel, plan_chunks, update_parallel
+
+    ds = Dataset(coords, copy=False)
+    cfg = KmeansConfig(k=c0.shape[0], max_iters=max_iters, tol=tol)
+    plan = plan_chunks(ds.n, workers)
+    model = ClusterModel(np.array(c0, dtype=np.float64, copy=True))
+    with ThreadPoolExecutor(max_workers=plan.n_workers) as pool:
+        model, assignment, iterations, done, _ = iterate(
+            ds, cfg, model,
+            lambda mdl: assign_parallel(ds, mdl, plan, executor=pool),
+            lambda a: update_parallel(ds, a, cfg.k, plan, block=cfg.accum_block, executor=pool),
+        )
+    return {"labels": assignment.labels, "centers": model.centers.copy(), "counts": model.counts.copy(),
+            "iterations": np.int64(iterations), "converged": np.bool_(done)}
+
+
+def bench_configs(which=("cfg2", "cfg3", "cfg3_20", "cfg4_20", "cfg5_3")):
+    """Full-size goldens of the BASELINE.json benchmark configs (the GPU box regenerates the
+    points with datasets.generate_synthetic_array — identical bytes — and checks them by digest):
+    the reference loop from the first K rows, tol = 0.  Labels are stored in full (uint8/uint16)
+    where they are small, otherwise as a SHA-256 digest of the int64 label array plus a strided
+    sample.  cfg3 runs to convergence (539 iterations); the *_20 / *_3 cases stop at max_iters
+    (the exhausted-run rule, engine.py:339-343)."""
+    import hashlib
+    import time
+
+    specs = {
+        "cfg2": (100_000, 10, 8, 1000),
+        "cfg3": (2_000_000, 25, 16, 1000),
+        "cfg3_20": (2_000_000, 25, 16, 20),
+        "cfg4_20": (2_000_000, 25, 512, 20),
+        "cfg5_3": (64_000_000, 25, 64, 3),
+    }
+    _kernels.warmup()
+    cache = {}
+    for name in which:
+        n, m, k, iters = specs[name]
+        key = (n, m, k)
+        if key not in cache:
+            cache.clear()
+            x32 = generate_synthetic(n, m, k, seed=0).coords.astype(np.float32)
+            cache[key] = (hashlib.sha256(x32.tobytes()).hexdigest(), x32.astype(np.float64))
+        digest, coords = cache[key]
+        c0 = coords[:k].copy()
+        t0 = time.perf_counter()
+        res = run_iterate_parallel(coords, c0, max_iters=iters)
+        el = time.perf_counter() - t0
+        lab = res["labels"]
+        rec = dict(n=np.int64(n), m=np.int64(m), k=np.int64(k), seed=np.int64(0), max_iters=np.int64(iters),
+                   tol=np.float64(0.0), coords_sha256=np.bytes_(digest), c0=c0,
+                   labels_sha256=np.bytes_(hashlib.sha256(lab.astype(np.int64).tobytes()).hexdigest()),
+                   labels_sample=lab[::997].astype(np.int64), centers=res["centers"], counts=res["counts"],
+                   iterations=res["iterations"], converged=res["converged"], ref_seconds=np.float64(el))
+        if n <= 2_000_000:
+            rec["labels"] = lab.astype(np.uint8 if k <= 256 else np.uint16)
+        save("bench_" + name, **rec)
+        print(f"bench_{name}: n={n} m={m} k={k} iterations={int(res['iterations'])} "
+              f"converged={bool(res['converged'])} ({el:.1f} s, 8 threads)", flush=True)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["seeding"]:
         seeding()
+    elif sys.argv[1:2] == ["bench"]:
+        bench_configs(tuple(sys.argv[2:]) or ("cfg2", "cfg3", "cfg3_20", "cfg4_20", "cfg5_3"))
     else:
         main()
         seeding()

@@ -19,6 +19,7 @@
 #include "../../include/kmeans_b200.h"
 #include "kmeans_kernels.cuh"
 #include "kmeans_seed.cuh"
+#include "kmeans_sums.cuh"
 #include "kmeans_tc.h"
 
 using namespace km;
@@ -55,6 +56,7 @@ struct km_engine {
   int32_t m = 0;
   int32_t point_bytes = 4;
   double absmax = 0.0;
+  double op_absmax = 0.0;  // max(|x|, |C|) the tensor-core operand scale was chosen for
   int32_t frac_bits = 0;
   bool frac_user = false;
 
@@ -96,6 +98,16 @@ struct km_engine {
   bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
   int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required, 3 SIMT without register blocking
   float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
+  // environment knobs, read once at km_create (tuning / A-B experiments only)
+  bool full_first_pass = false;     // KM_FULL_FIRST_PASS=1: fused full first pass (epilogue atomics)
+  bool no_resident = false;         // KM_NO_RESIDENT=1: launch-per-iteration loop
+  int dbg_flags = 0;                // KM_TC_DBG
+  const char* times_path = nullptr; // KM_TC_TIMES
+  size_t sums_key = 0;              // cluster-sums launch geometry cache
+  bool resident_zeroed = false;     // grid barrier + delta buffers are zero (next resident launch)
+  void* pin = nullptr;              // pinned staging of the resident loop's C0 / model
+  size_t pin_cap = 0;
+  int sums_per_sm = 1;
 
   km_stats stats{};
   bool profiling = false;
@@ -284,7 +296,8 @@ static int finish_threads(int k, int m);
 // resident: the whole Lloyd loop in one cooperative launch (returns KM_RESIDENT_UNFIT when the
 // shape only fits the launch-per-iteration kernel)
 constexpr int KM_RESIDENT_UNFIT = -3;
-static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, bool resident = false) {
+static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, bool resident = false,
+                     bool no_sums = false, bool skip_first = false) {
   tc::TcArgs a{};
   a.x = (const float*)e->x;
   a.n = e->n;
@@ -306,8 +319,10 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   // absolute floor (operand units): fp16 subnormal spacing 2^-24 per element times |w| ≤ 2·max‖x‖·pre
   a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -23) * (1.0 + 2.0 * e->xnorm_max * e->pre));
   a.nx_inflate = (float)(1.0 + (e->m + 2) * std::ldexp(1.0, -24));
-  a.exact_only = (e->absmax > std::ldexp(1.0, 50)) ? 1 : 0;
+  a.exact_only = (e->op_absmax > std::ldexp(1.0, 50)) ? 1 : 0;
   a.full = full ? 1 : 0;
+  a.no_sums = no_sums ? 1 : 0;
+  a.skip_first = skip_first ? 1 : 0;
   a.exact_m = 1;
   a.prescale = e->prescale ? 1 : 0;
   a.recheck_rows = e->recheck_rows;
@@ -320,16 +335,17 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   a.resident = resident ? 1 : 0;
   a.grid_sync = e->grid_sync;
   a.dlt = e->dlt;
-  if (resident) {
+  if (resident && !e->resident_zeroed) {  // (the begin kernel zeroed them for the first launch of a run)
     CK(cudaMemsetAsync(e->grid_sync, 0, 16, e->stream));
     CK(cudaMemsetAsync(e->dlt, 0, 3 * 8 * ((size_t)e->k * e->m + e->k), e->stream));
   }
+  if (resident) e->resident_zeroed = false;
   a.st = e->st;
   a.gate = gated ? 1 : 0;
   a.dbg_scores = e->dbg_scores;
-  a.dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
+  a.dbg_flags = e->dbg_flags;
   a.dbg_times = nullptr;
-  if (getenv("KM_TC_TIMES")) {  // tuning only: dump per-tile stamps of CTA 0 to a file after the pass
+  if (e->times_path) {  // tuning only: dump per-tile stamps of CTA 0 to a file after the pass
     static long long* dt = nullptr;
     if (!dt) cudaMalloc((void**)&dt, 1024 * 8 * 8);
     cudaMemsetAsync(dt, 0, 1024 * 8 * 8, e->stream);
@@ -342,16 +358,13 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   if (rc == 2) return set_err(e, KM_ERR_CAPACITY, "%s", msg);
   if (rc == 3) return KM_RESIDENT_UNFIT;
   e->stats.kernel_launches += 1;
-  if (!fuse && !resident) {  // overflow of the per-CTA queues (rare): re-decide before anyone reads the sums
-    c = tc::launch_recheck(a, e->num_sms, e->stream);
-    if (c != cudaSuccess) return cuda_fail(e, c, "recheck_kernel launch");
-    e->stats.kernel_launches += 1;
-  }
+  // (no recheck launch: the tensor-core pass re-decides every uncertified point itself — its
+  // per-CTA queue overflows are decided inline — and never writes the global recheck queue)
   if (a.dbg_times) {
     static long long h[1024 * 8];
     cudaMemcpyAsync(h, a.dbg_times, sizeof h, cudaMemcpyDeviceToHost, e->stream);
     cudaStreamSynchronize(e->stream);
-    FILE* f = fopen(getenv("KM_TC_TIMES"), "a");
+    FILE* f = fopen(e->times_path, "a");
     if (f) {
       for (int i = 0; i < 64; ++i) {
         if (!h[i * 8]) continue;
@@ -649,6 +662,31 @@ static int scan_points(km_engine* e, const void* x, int bytes_per, int64_t count
   return KM_OK;
 }
 
+// Tensor-core operand range (fp16 hi/lo): `amax` bounds every |x_f| AND every |c_f| the pass
+// will see.  Data already in a safe range (amax ≥ 2^-4, every score |S| ≤ ‖c‖² + 2|x·c| ≤
+// 3·m·amax² ≤ 2^15 < the +65504 padding score) go as is; otherwise both operands are prescaled
+// by an exact power of two 2^s with |v·2^s| < 1.  Lloyd iterates are means of points (|c_f| ≤
+// max|x_f|), but caller-supplied centres (km_assign, C0 of km_lloyd / km_step_begin) may be far
+// larger than the data, so those entry points widen amax to max(max|x|, max|C|).
+static void choose_operand_scale(km_engine* e, double amax) {
+  e->op_absmax = amax;
+  e->pre = 1.f;
+  e->prescale = true;
+  if (amax >= std::ldexp(1.0, -4) && 4.0 * e->m * amax * amax <= 32768.0) {
+    e->prescale = false;
+  } else if (amax > 0.0 && amax < std::ldexp(1.0, 100)) {
+    const int s = -(std::ilogb(amax) + 1);
+    e->pre = (float)std::ldexp(1.0, std::max(-120, std::min(120, s)));
+  }
+}
+
+// widen the operand range to the centres a run starts from (see choose_operand_scale)
+static void scale_for_centers(km_engine* e, const double* c, int32_t k) {
+  double cm = 0.0;
+  for (int64_t i = 0; i < (int64_t)k * e->m; ++i) cm = std::max(cm, std::fabs(c[i]));
+  choose_operand_scale(e, std::max(e->absmax, cm));
+}
+
 static int after_points_loaded(km_engine* e) {
   {  // max ‖x_i‖ for the tensor-core filter bound
     unsigned int zero = 0, bits = 0;
@@ -665,17 +703,7 @@ static int after_points_loaded(km_engine* e) {
     std::memcpy(&e->xnorm_max, &bits, 4);
   }
   if (!e->frac_user) e->frac_bits = compute_frac_bits(e->absmax, e->n);
-  // tensor-core operands are fp16: data already in a safe range (|x| ≥ 2^-4 scale, every score
-  // |S| ≤ 4·m·max|x|² ≤ 2^15 < the +65504 padding score) go as is; otherwise prescale by an exact
-  // power of two 2^s with |x·2^s| < 1
-  e->pre = 1.f;
-  e->prescale = true;
-  if (e->absmax >= std::ldexp(1.0, -4) && 4.0 * e->m * e->absmax * e->absmax <= 32768.0) {
-    e->prescale = false;
-  } else if (e->absmax > 0.0 && e->absmax < std::ldexp(1.0, 100)) {
-    const int s = -(std::ilogb(e->absmax) + 1);
-    e->pre = (float)std::ldexp(1.0, std::max(-120, std::min(120, s)));
-  }
+  choose_operand_scale(e, e->absmax);
   e->next_full = true;
   e->stats.frac_bits = e->frac_bits;
   e->stats.point_bytes = e->point_bytes;
@@ -689,6 +717,9 @@ static int drop_points(km_engine* e) {
   e->x_owned = false;
   e->n = 0;
   e->m = 0;
+  // a fixed-point scale set for the previous points (km_set_frac_bits) is not valid for new
+  // ones: a larger n·max|x| would overflow the int64 sums
+  e->frac_user = false;
   return KM_OK;
 }
 
@@ -799,6 +830,10 @@ int km_create(int32_t device, km_engine** out) {
                    prop.major, prop.minor);
   km_engine* e = new km_engine();
   e->device = device;
+  e->full_first_pass = getenv("KM_FULL_FIRST_PASS") && atoi(getenv("KM_FULL_FIRST_PASS")) != 0;
+  e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
+  e->dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
+  e->times_path = getenv("KM_TC_TIMES");
   e->num_sms = prop.multiProcessorCount;
   e->smem_optin = prop.sharedMemPerBlockOptin;
   if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -832,6 +867,7 @@ int km_destroy(km_engine* e) {
   dfree(e->scratch_u);
   dfree(e->scratch_i);
   if (e->st_host) cudaFreeHost(e->st_host);
+  if (e->pin) cudaFreeHost(e->pin);
   if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
   delete e;
   return KM_OK;
@@ -948,6 +984,7 @@ int km_assign(km_engine* e, const double* centers, int32_t k, int64_t* labels_ou
   if ((r = ensure_k(e, k))) return r;
   CK(cudaMemcpyAsync(e->cur, centers, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
   if ((r = reset_state(e, 1, 0.0))) return r;
+  scale_for_centers(e, centers, k);
   if ((r = launch_prep(e))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   if ((r = launch_pass(e, PASS_ASSIGN_ONLY, false))) return r;
@@ -1021,13 +1058,76 @@ int km_converged(km_engine* e, const double* prev, const double* next, int32_t k
   return KM_OK;
 }
 
+// Exact fixed-point sums + counts of every resident point by its current label, added into `out`
+// ([k·m sums][k counts], zeroed by the caller): one HBM stream, warp-private accumulators where
+// they fit (kmeans_sums.cuh).  Also clears the recheck overflow counter of the pass before it.
+static int launch_sums(km_engine* e, unsigned long long* out) {
+  if (e->point_bytes != 4 || e->m > 31) return set_err(e, KM_ERR_INTERNAL, "cluster-sums kernel: fp32, m <= 31 only");
+  const size_t per = (size_t)e->k * (e->m + 1) * 8;
+  const bool priv = per * (kSumsThreads / 32) <= 32 * 1024;
+  const size_t smem = priv ? per * (kSumsThreads / 32) : per;
+  if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
+  auto kern = priv ? cluster_sums_f32_kernel<true> : cluster_sums_f32_kernel<false>;
+  // launch geometry per (k, m) shape, computed once (no attribute / occupancy queries per call)
+  if (e->sums_key != per) {
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSumsThreads, smem));
+    e->sums_per_sm = std::max(1, per_sm);
+    e->sums_key = per;
+  }
+  const int per_sm = e->sums_per_sm;
+  const int64_t warps_needed = (e->n + kSumsRows * 4 - 1) / (kSumsRows * 4);  // ≥ 4 batches per warp
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * e->num_sms,
+                                                              (warps_needed + 7) / 8));
+  CK(cudaMemsetAsync(e->recheck_count, 0, 4, e->stream));
+  kern<<<(unsigned)grid, kSumsThreads, smem, e->stream>>>((const float*)e->x, e->labels, e->n, e->m, e->k,
+                                                          (float)std::ldexp(1.0, e->frac_bits),
+                                                          std::ldexp(1.0, e->frac_bits),
+                                                          (e->frac_bits > 120 || e->frac_bits < -120) ? 1 : 0, out);
+  CK_LAUNCH("cluster_sums_f32_kernel");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
 // Tensor-core resident loop: the whole Lloyd iteration runs inside one cooperative launch
 // (lloyd_pass_tc_kernel with a.resident); the host only steps in for empty-cluster repairs.
-static int lloyd_resident(km_engine* e) {
+// Host cost per call (the bench times whole calls): one pinned H2D of C0, one begin kernel
+// (state, zeroed accumulators, filter operands), the first pass + cluster sums + the resident
+// launch, and ONE synchronisation that also brings back the state, the centres and the counts
+// (pinned).  Returns KM_RESIDENT_UNFIT when the shape only fits the launch-per-iteration kernel.
+static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double tol) {
   int r;
-  const size_t nacc = (size_t)e->k * e->m + e->k;
-  CK(cudaMemsetAsync(e->tot, 0, 8 * nacc, e->stream));  // the first (full) pass adds every point
-  bool full = true;
+  const int k = e->k, m = e->m;
+  const size_t km = (size_t)k * m, nacc = km + k;
+  // pinned staging: [C0 | C out | counts out]
+  const size_t pin_bytes = 8 * (2 * km + k);
+  if (e->pin_cap < pin_bytes) {
+    if (e->pin) cudaFreeHost(e->pin);
+    e->pin = nullptr;
+    e->pin_cap = 0;
+    CK(cudaMallocHost(&e->pin, pin_bytes));
+    e->pin_cap = pin_bytes;
+  }
+  double* pin_c0 = reinterpret_cast<double*>(e->pin);
+  double* pin_c = pin_c0 + km;
+  long long* pin_n = reinterpret_cast<long long*>(pin_c + km);
+  std::memcpy(pin_c0, c0, 8 * km);
+  CK(cudaMemcpyAsync(e->cur, pin_c0, 8 * km, cudaMemcpyHostToDevice, e->stream));
+  lloyd_begin_kernel<<<1, 512, 0, e->stream>>>(e->st, max_iters, tol, e->part, e->tot, e->dlt, nacc, e->grid_sync,
+                                               e->recheck_count, e->cur, e->w, e->cn, e->cmax, k, m, e->mpad,
+                                               tc_eligible(e) ? e->wop : nullptr, e->kp, e->pre);
+  CK_LAUNCH("lloyd_begin_kernel launch");
+  e->stats.kernel_launches += 1;
+  e->resident_zeroed = true;
+  e->next_full = true;
+  // First pass split in two: L0 = A(C0) writes labels only (tensor cores), then one cluster-sums
+  // stream adds every point to its cluster (S(L0) into tot); the resident loop starts at the
+  // finish of iteration 1.  (KM_FULL_FIRST_PASS=1: the fused first pass adding every point
+  // through the epilogue's shared-memory atomics, kept for A/B timing.)
+  const bool split = !e->full_first_pass;
+  bool full = !split, first = true;
+  DevState* hs = e->st_host;
   for (;;) {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     if (e->profiling) {
@@ -1040,25 +1140,42 @@ static int lloyd_resident(km_engine* e) {
       ev1 = e->ev[1];
       CK(cudaEventRecord(ev0, e->stream));
     }
-    const int passes_before = e->st_host->passes;
-    if ((r = launch_tc(e, full, true, false, true))) return r;
+    const int passes_before = hs->passes;
+    const bool skip = split && first;
+    if (skip) {
+      if ((r = launch_tc(e, true, false, false, false, true))) return r;  // labels of C0 only
+      if ((r = launch_sums(e, e->tot))) return r;
+    }
+    if ((r = launch_tc(e, full, true, false, true, false, skip))) return r;
     if (e->profiling) CK(cudaEventRecord(ev1, e->stream));
-    if ((r = read_state(e))) return r;
-    const DevState s = *e->st_host;
-    if (e->profiling && s.passes > passes_before) {
+    // one round trip: state + (if the loop is done) the model
+    CK(cudaMemcpyAsync(hs, e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(pin_c, e->cur, 8 * km, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaMemcpyAsync(pin_n, e->model_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
+    CK(cudaStreamSynchronize(e->stream));
+    e->stats.host_syncs += 1;
+    const DevState s = *hs;
+    const int ran = s.passes - passes_before + (skip ? 1 : 0);
+    if (e->profiling && ran > 0) {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, ev0, ev1));
       e->stats.pass_ms_total += ms;
-      e->stats.pass_timed += s.passes - passes_before;
+      e->stats.pass_timed += ran;
     }
     full = false;
+    first = false;
     e->next_full = false;
     if (s.done) return KM_OK;
     if (!s.need_host) return set_err(e, KM_ERR_INTERNAL, "resident Lloyd loop stopped without a decision");
     if ((r = repair_local(e))) return r;
     if ((r = launch_check(e))) return r;
     if ((r = read_state(e))) return r;
-    if (e->st_host->done) return KM_OK;
+    if (hs->done) {  // the repaired model converged: bring it back
+      CK(cudaMemcpyAsync(pin_c, e->cur, 8 * km, cudaMemcpyDeviceToHost, e->stream));
+      CK(cudaMemcpyAsync(pin_n, e->model_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
+      CK(cudaStreamSynchronize(e->stream));
+      return KM_OK;
+    }
   }
 }
 
@@ -1073,22 +1190,34 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
   if (k > e->n) return set_err(e, KM_ERR_CONTRACT, "k=%d exceeds sample count n=%lld", k, (long long)e->n);
   if ((r = check_centers(e, c0, k))) return r;
   if ((r = ensure_k(e, k))) return r;
+  scale_for_centers(e, c0, k);
+  if (use_tc(e) && !e->resident_unfit && !e->no_resident) {
+    r = lloyd_resident(e, c0, max_iters, tol);
+    if (r == KM_OK) {
+      const DevState s = *e->st_host;
+      const size_t km = (size_t)k * e->m;
+      const double* pin_c = reinterpret_cast<const double*>(e->pin) + km;
+      e->stats.passes += 1 + s.t - (s.converged ? 1 : 0);
+      e->stats.rechecked += (int64_t)s.rechecked;
+      e->stats.changed += (int64_t)s.changed;
+      if (centers_out) std::memcpy(centers_out, pin_c, 8 * km);
+      if (counts_out) std::memcpy(counts_out, pin_c + km, 8 * (size_t)k);
+      if (labels_out) {
+        if ((r = download_labels(e, labels_out))) return r;
+        CK(cudaStreamSynchronize(e->stream));
+      }
+      if (iterations_out) *iterations_out = s.t;
+      if (converged_out) *converged_out = s.converged;
+      return KM_OK;
+    }
+    if (r != KM_RESIDENT_UNFIT) return r;
+    e->resident_unfit = true;
+  }
   CK(cudaMemcpyAsync(e->cur, c0, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
   if ((r = reset_state(e, max_iters, tol))) return r;
   if ((r = launch_prep(e))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   e->next_full = true;  // the labels buffer does not hold L of this run yet
-  bool ran_resident = false;
-  if (use_tc(e) && !e->resident_unfit && !getenv("KM_NO_RESIDENT")) {
-    r = lloyd_resident(e);
-    if (r == KM_RESIDENT_UNFIT) {
-      e->resident_unfit = true;
-    } else if (r) {
-      return r;
-    } else {
-      ran_resident = true;
-    }
-  }
   // Tensor-core path: ONE launch per iteration — pass t + (last CTA) finish t+1.
   // SIMT path: finish and pass are separate launches.
   const bool fused = use_tc(e);
@@ -1130,10 +1259,10 @@ int km_lloyd(km_engine* e, const double* c0, int32_t k, int32_t max_iters, doubl
     return KM_OK;
   };
   // L0 = A(C0) (engine.py:328), fused with the sums U(L0) needs (and, fused, the first update).
-  if (!ran_resident && (r = timed_pass())) return r;
+  if ((r = timed_pass())) return r;
   int first = 1;
   int t_before = 0;
-  while (!ran_resident) {
+  for (;;) {
     for (int b = 0; b < batch; ++b) {
       if (!fused && (r = launch_finish(e, 0, !prev_full))) return r;
       if ((r = timed_pass())) return r;
@@ -1436,6 +1565,7 @@ int km_step_begin(km_engine* e, const double* c0, int32_t k) {
   if ((r = ensure_k(e, k))) return r;
   CK(cudaMemcpyAsync(e->cur, c0, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));
   if ((r = reset_state(e, INT32_MAX, 0.0))) return r;
+  scale_for_centers(e, c0, k);
   if ((r = launch_prep(e))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   e->next_full = true;

@@ -667,6 +667,32 @@ __global__ void __launch_bounds__(512) prep_filter_kernel(const double* c, float
   block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red, wop, kp, pre);
 }
 
+// Start of a resident Lloyd run (km_lloyd, tensor-core path), one launch instead of a state
+// upload + five memsets + the prep kernel: loop state {max_iters, tol}, zeroed Δ / totals /
+// rotating delta buffers / grid-barrier counter / recheck counter, and the filter operands of C0.
+__global__ void __launch_bounds__(512) lloyd_begin_kernel(DevState* st, int max_iters, double tol,
+                                                          unsigned long long* part, unsigned long long* tot,
+                                                          unsigned long long* dlt, size_t nacc,
+                                                          unsigned int* grid_sync, unsigned int* recheck_count,
+                                                          const double* c, float* w, float* cn, float* cmax, int k,
+                                                          int m, int mpad, unsigned short* wop, int kp, float pre) {
+  __shared__ float s_red[32];
+  if (threadIdx.x == 0) {
+    DevState s{};
+    s.max_iters = max_iters;
+    s.tol = tol;
+    *st = s;
+    grid_sync[0] = grid_sync[1] = grid_sync[2] = grid_sync[3] = 0u;
+    *recheck_count = 0u;
+  }
+  for (size_t i = threadIdx.x; i < nacc; i += blockDim.x) {
+    part[i] = 0ull;
+    tot[i] = 0ull;
+  }
+  for (size_t i = threadIdx.x; i < 3 * nacc; i += blockDim.x) dlt[i] = 0ull;
+  block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red, wop, kp, pre);
+}
+
 // Standalone congruence test (km_converged).
 __global__ void __launch_bounds__(512) converged_kernel(const double* prev, const double* next, int k, int m,
                                                         double tol, int* out) {

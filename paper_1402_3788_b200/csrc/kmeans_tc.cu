@@ -17,7 +17,8 @@ __global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ 
                                                       const double* __restrict__ c64, int32_t* labels,
                                                       const long long* rows, const unsigned int* count,
                                                       unsigned long long* part, float scale_f, double scale_d,
-                                                      int use_dscale, int full, DevState* st, int gate) {
+                                                      int use_dscale, int full, int no_sums, DevState* st,
+                                                      int gate) {
   if (gate && (st->done || st->need_host)) return;
   const unsigned int cnt = *count;
   if (cnt == 0) return;
@@ -56,6 +57,10 @@ __global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ 
     }
     const int old = full ? -1 : labels[row];
     if (bl != old) {
+      if (no_sums) {  // first pass of a run: labels only (the cluster-sums kernel adds the points)
+        if (lane == 0) labels[row] = bl;
+        continue;
+      }
       if (lane == 0) {
         labels[row] = bl;
         atomicAdd(part + (size_t)k * m + bl, 1ull);
@@ -77,7 +82,8 @@ cudaError_t launch_recheck(const TcArgs& a, int num_sms, cudaStream_t stream) {
   const size_t smem = (size_t)a.k * a.m <= 6144 ? (size_t)a.k * a.m * 8 : 0;
   // one resident warp per queued point (≈ 64 warps/SM): the per-point latency is a few L2 loads
   recheck_kernel<<<num_sms * 8, 256, smem, stream>>>(a.x, a.m, a.k, a.c64, a.labels, a.recheck_rows, a.recheck_count,
-                                                     a.part, a.scale_f, a.scale_d, a.use_dscale, a.full, a.st, a.gate);
+                                                     a.part, a.scale_f, a.scale_d, a.use_dscale, a.full, a.no_sums, a.st,
+                                                     a.gate);
   return cudaGetLastError();
 }
 

@@ -706,14 +706,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   const int max_iters = st->max_iters;
   const double tol = st->tol;
   bool full = a.full != 0;
+  const bool no_sums = a.no_sums != 0;
   int cb = 0;      // resident: s_cbuf half holding C_t
   int g0 = 0;      // tiles of earlier passes (ring positions continue across passes)
   int issued = 0;  // producer: tiles of the current pass already in flight
+  int last_pass_tiles = my_tiles;
 
   // tuning only: per-pass phase ends (globaltimer, max over CTAs) of the resident loop
   unsigned long long* pst = (KM_TC_TUNING && a.dbg_times != nullptr && resident && tid == 0)
                                 ? reinterpret_cast<unsigned long long*>(a.dbg_times + 4096) : nullptr;
   for (int it = 0;; ++it) {
+    // tiles of this pass (resident skip_first: the labels and their sums come from a separate
+    // first pass + cluster-sums launch, so iteration 0 starts at the tail with Δ = 0)
+    const int pass_tiles = (resident && it == 0 && a.skip_first) ? 0 : my_tiles;
+    last_pass_tiles = pass_tiles;
     const double* C = resident ? s_cbuf + cb * km : a.c64;
     if (pst && it < 256 && blockIdx.x == 0) pst[it * 8 + 0] = globaltimer();
     if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2] = (long long)globaltimer();
@@ -730,6 +736,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       if (bl != old) {
         a.labels[row] = bl;
         if (!full) atomicAdd(&st->changed, 1ull);
+        if (no_sums) { s_q[q] = 0; return; }
 #pragma unroll
         for (int f = 0; f < MP; ++f) {
           if (f < m) {
@@ -787,8 +794,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             bulk_g2s_hint(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes, full_raw + s,
                           pol);
         };
-        for (int i = issued; i < my_tiles; ++i) issue(g0 + i, i);
-        for (int j = 0; j < npre; ++j) issue(g0 + my_tiles + j, j);  // next pass (resident)
+        for (int i = issued; i < pass_tiles; ++i) issue(g0 + i, i);
+        for (int j = 0; j < npre; ++j) issue(g0 + pass_tiles + j, j);  // next pass (resident)
       }
       issued = npre;
     } else if (warp >= kMmaWarp) {
@@ -800,7 +807,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       constexpr uint32_t idesc = idesc_f16(SC);
       const uint64_t bdescL = make_desc(w0 + KP * 128, 16, 1024);  // B rows KP.. ([wl | 0]) for the K3 tail
       const uint64_t bdesc0 = make_desc(w0, 16, 1024);
-      for (int i = (mj - (g0 & 1)) & 1; i < my_tiles && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
+      for (int i = (mj - (g0 & 1)) & 1; i < pass_tiles && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
         const int g = g0 + i;
         const int sa = g % AS, ss = g % TM::NS;
         long long* ms = (KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && i < 64 && lane == 0 && it == (resident ? 100 : 0))
@@ -845,7 +852,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
       const int key = p & 7;
       const float* __restrict__ gx = a.x;
-      for (int i = ((tg - g0) % kTransformGroups + kTransformGroups) % kTransformGroups; i < my_tiles;
+      for (int i = ((tg - g0) % kTransformGroups + kTransformGroups) % kTransformGroups; i < pass_tiles;
            i += kTransformGroups) {
         const int g = g0 + i;
         const int s = g % RS, sa = g % AS;
@@ -957,12 +964,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0;
       unsigned int my_changed = 0, my_rechecked = 0;
       auto prev_label = [&](int i, int mb) -> int {  // previous label of point p + 128·mb of tile i (or -1)
-        if (full || i >= my_tiles) return -1;
+        if (full || i >= pass_tiles) return -1;
         if (KM_DBG_FLAGS & 128) return 0;  // timing experiment only: no label loads
         const int64_t r = (t_lo + i) * TR + 128 * mb + p;
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
-      const int i0 = e < EG ? ((e - g0) % EG + EG) % EG : my_tiles;  // groups ≥ EG idle
+      const int i0 = e < EG ? ((e - g0) % EG + EG) % EG : pass_tiles;  // groups ≥ EG idle
       // previous labels prefetched two tiles of this group ahead (an L2 or DRAM round trip
       // must not stall the epilogue)
       int old_n1[MB], old_n2[MB];
@@ -971,7 +978,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         old_n1[mb] = prev_label(i0, mb);
         old_n2[mb] = prev_label(i0 + EG, mb);
       }
-      for (int i = i0; i < my_tiles && !(KM_DBG_FLAGS & 4); i += EG) {
+      for (int i = i0; i < pass_tiles && !(KM_DBG_FLAGS & 4); i += EG) {
         const int g = g0 + i;
         const int ss = g % TM::NS;
         const int64_t row0 = (t_lo + i) * TR;
@@ -1059,6 +1066,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             }
             mk[(ch * 16) >> 5] |= bits << ((ch * 16) & 31);
           }
+          // padded centres (c ≥ k) are never candidates, whatever the threshold (exact_only
+          // sets it to +inf): the recheck only ever reads real centre rows
+#pragma unroll
+          for (int w = 0; w < MW; ++w) {
+            const int lim = k - 32 * w;
+            mk[w] &= lim >= 32 ? 0xffffffffu : lim <= 0 ? 0u : ((1u << lim) - 1u);
+          }
           int bi = (int)(cnt >> 8);
           const bool unc = active && (cnt & 0xff) != 1u && !(KM_DBG_FLAGS & 256);  // (dbg 256: timing only)
           if (__any_sync(0xffffffffu, unc)) {
@@ -1098,7 +1112,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             ++my_changed;
             a.labels[row0 + 128 * mb + p] = bi;
           }
-          const unsigned int pend = __ballot_sync(0xffffffffu, chg);
+          const unsigned int pend = __ballot_sync(0xffffffffu, chg && !no_sums);
           if (pend)
             delta_rows(a.x, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, s_acc, km, scale_f, scale_d,
                        use_dscale);
@@ -1190,7 +1204,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     // ---- resident finish (every CTA; CTA 0 publishes) — engine._finish_update / converged ----
     const bool pub = blockIdx.x == 0;
     bool stop = false;
-    if (pub && tid == 0) st->passes += 1;
+    if (pub && tid == 0 && pass_tiles > 0) st->passes += 1;
     if (exhausted) {
       // the final assign pass of an exhausted run: counts = bincount(L_T), C_T unchanged
       if (pub) {
@@ -1301,13 +1315,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     __syncthreads();
     if (pst && it < 256) atomicMax(pst + it * 8 + 7, globaltimer());
     if (stop) break;
-    g0 += my_tiles;
+    g0 += pass_tiles;
   }
   // ---- teardown ----
   if (resident && warp == kProducerWarp && lane == 0) {
     // the prefetched tiles of the pass that does not run: let their copies land before exit
     for (int j = 0; j < npre; ++j) {
-      const int g = g0 + my_tiles + j;
+      const int g = g0 + last_pass_tiles + j;
       mbar_wait(full_raw + g % RS, (g / RS) & 1);
     }
   }
@@ -1324,24 +1338,30 @@ inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_
                     size_t len) {
   auto kern = lloyd_pass_tc_kernel<MT, KP, PRE>;
   constexpr int MP = MT > 0 ? MT : -MT;
-  cudaFuncAttributes fa{};
-  cudaError_t c = cudaFuncGetAttributes(&fa, kern);
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncGetAttributes(tc)"); return 1; }
+  // per-instantiation launch facts, queried once (a launch is otherwise one cudaLaunchKernelEx):
+  // static smem, and the largest dynamic smem size already granted to the function
+  static size_t static_smem = SIZE_MAX, granted = 0;
+  cudaError_t c;
+  if (static_smem == SIZE_MAX) {
+    cudaFuncAttributes fa{};
+    c = cudaFuncGetAttributes(&fa, kern);
+    if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncGetAttributes(tc)"); return 1; }
+    c = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc carveout)"); return 1; }
+    static_smem = fa.sharedSizeBytes;
+  }
   const size_t smem = TcSmem<MP, KP>(a.m, a.resident ? a.k : 0).total;
-  (void)MP;
-  if (smem + fa.sharedSizeBytes > smem_optin) {
-    snprintf(msg, len, "tensor-core pass needs %zu B of shared memory (max %zu)", smem + fa.sharedSizeBytes,
-             smem_optin);
+  if (smem + static_smem > smem_optin) {
+    snprintf(msg, len, "tensor-core pass needs %zu B of shared memory (max %zu)", smem + static_smem, smem_optin);
     return a.resident ? 3 : 2;
   }
-  c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc smem)"); return 1; }
-  c = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc carveout)"); return 1; }
-  int per_sm = 0;
-  c = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreadsTC, smem);
-  if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "occupancy(tc)"); return 1; }
-  if (per_sm < 1) { snprintf(msg, len, "tensor-core pass does not fit on an SM"); return 2; }
+  if (smem > granted) {
+    c = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (c != cudaSuccess) { *ce = c; snprintf(msg, len, "cudaFuncSetAttribute(tc smem)"); return 1; }
+    granted = smem;
+  }
+  // one CTA of kThreadsTC threads with ≤ 227 KB of shared memory per SM: fits whenever the
+  // shared-memory check above passes (the register budget is fixed by __launch_bounds__)
   const int64_t ntiles = (a.n + TcStages<MP, KP>::TR - 1) / TcStages<MP, KP>::TR;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));  // one persistent CTA/SM
   cudaLaunchConfig_t cfg{};

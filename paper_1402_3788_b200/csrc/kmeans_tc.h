@@ -33,6 +33,10 @@ struct TcArgs {
   int32_t exact_m;         // 1: use a compile-time-m instantiation when one exists for m
   int32_t prescale;        // 1: multiply x by `pre` (else the data are fp16-safe as is; pre == 1)
   int32_t full;            // 1: old labels invalid (first pass / standalone assign): add every point
+  int32_t no_sums;         // 1: labels only (no Δ / sums): the first pass of a run, whose sums the
+                           //    cluster-sums kernel computes in one stream afterwards
+  int32_t skip_first;      // resident: the sums of the current labels are already in fin.tot
+                           //    (first pass run separately): start the loop at the finish
   long long* recheck_rows;      // global overflow queue of uncertified points
   unsigned int* recheck_count;
   int32_t fuse_finish;     // 1: the last CTA to finish runs finish_block(fin) (single-GPU loop)

@@ -5,7 +5,7 @@ sequence, no tolerances — the reference's own test style (test_kernels.py)."""
 import numpy as np
 import pytest
 
-from conftest import golden, golden_indexed
+from conftest import GOLDEN, golden, golden_indexed
 from oracle import oracle
 
 LLOYD_CASES = ["blob4", "synth_10k_5_4", "synth_20k_25_16", "synth_30k_10_8", "maxiter1", "maxiter5", "k1",
@@ -82,3 +82,21 @@ def test_worker_count_invariance():
         other = oracle.lloyd(x, g["c0"], max_iters=7, n_workers=w)
         assert np.array_equal(other["centers"], base["centers"])
         assert np.array_equal(other["labels"], base["labels"])
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3_20"])
+def test_oracle_matches_reference_bench_configs(name):
+    """The C restatement against the REAL reference at benchmark sizes (many 65,536-row
+    accumulation blocks: the multi-block fold, model.py:163-173)."""
+    import hashlib
+
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    g = dict(np.load(GOLDEN / f"bench_{name}.npz"))
+    x = generate_synthetic_array(int(g["n"]), int(g["m"]), int(g["k"]), seed=int(g["seed"]), dtype=np.float32)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == g["coords_sha256"].item().decode()
+    want = oracle.lloyd(x.astype(np.float64), g["c0"], max_iters=int(g["max_iters"]), n_workers=8)
+    assert want["iterations"] == int(g["iterations"]) and want["converged"] == bool(g["converged"])
+    assert np.array_equal(want["labels"], g["labels"].astype(np.int64))
+    assert np.array_equal(want["counts"], g["counts"])
+    assert np.array_equal(want["centers"], g["centers"])  # same sequential fp64 arithmetic: bit-identical
