@@ -1140,7 +1140,7 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
       ev1 = e->ev[1];
       CK(cudaEventRecord(ev0, e->stream));
     }
-    const int passes_before = hs->passes;
+    const int passes_before = first ? 0 : hs->passes;  // (the begin kernel zeroed the device state)
     const bool skip = split && first;
     if (skip) {
       if ((r = launch_tc(e, true, false, false, false, true))) return r;  // labels of C0 only

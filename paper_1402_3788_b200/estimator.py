@@ -10,6 +10,8 @@ fallback: a missing or lost device raises.
 from __future__ import annotations
 
 import numpy as np
+from sklearn.base import BaseEstimator, ClusterMixin
+from sklearn.utils.validation import check_is_fitted
 
 from .engine import KmeansConfig, run_b200
 from .exceptions import ContractViolationError
@@ -17,9 +19,14 @@ from .model import DEFAULT_BLOCK, ClusterModel, Dataset, wcss
 from .validation import check_coordinates
 
 
-class RegimeKMeans:
+class RegimeKMeans(ClusterMixin, BaseEstimator):
     """K-means with the reference's seeding (diameter + maximin / random-far) and
-    Lloyd iteration, bit-compatible labels and iteration counts."""
+    Lloyd iteration, bit-compatible labels and iteration counts.
+
+    A scikit-learn estimator like the reference's (estimator.py:19): ``get_params`` /
+    ``set_params`` / ``clone`` come from ``BaseEstimator`` (constructor introspection),
+    ``fit_predict`` from ``ClusterMixin``, and an unfitted ``predict`` / ``transform``
+    raises sklearn's ``NotFittedError`` (``check_is_fitted``, estimator.py:177,185)."""
 
     def __init__(self, n_clusters=8, *, regime="auto", n_workers=None, device="b200", init="maximin",
                  max_iter=1000, tol=0.0, random_state=0, auto_prefer="gpu", accum_block=DEFAULT_BLOCK,
@@ -36,16 +43,6 @@ class RegimeKMeans:
         self.accum_block = accum_block
         self.diameter_pair_cap = diameter_pair_cap
         self.track_wcss = track_wcss
-
-    def get_params(self, deep=True):
-        return {k: getattr(self, k) for k in ("n_clusters", "regime", "n_workers", "device", "init", "max_iter",
-                                              "tol", "random_state", "auto_prefer", "accum_block",
-                                              "diameter_pair_cap", "track_wcss")}
-
-    def set_params(self, **params):
-        for k, v in params.items():
-            setattr(self, k, v)
-        return self
 
     def _config(self):
         return KmeansConfig(k=self.n_clusters, max_iters=self.max_iter, tol=self.tol,
@@ -76,10 +73,6 @@ class RegimeKMeans:
         self.fallback_reason_ = result.fallback_reason
         return self
 
-    def _check_fitted(self):
-        if not hasattr(self, "cluster_centers_"):
-            raise ContractViolationError("this RegimeKMeans instance is not fitted yet; call fit first")
-
     def _check_input(self, X):
         arr = check_coordinates(X, name="X")
         if arr.shape[1] != self.n_features_in_:
@@ -89,7 +82,7 @@ class RegimeKMeans:
 
     def predict(self, X):
         """Nearest-centre label per sample, ties toward the lower index (estimator.py:175-181)."""
-        self._check_fitted()
+        check_is_fitted(self, "cluster_centers_")
         arr = self._check_input(X)
         ds = Dataset(arr)
         labels, _ = ds.device_engine(self._device_index()).assign(self.cluster_centers_)
@@ -97,12 +90,9 @@ class RegimeKMeans:
 
     def transform(self, X):
         """Distance from each sample to each centre, shape (n, k) (estimator.py:183-189)."""
-        self._check_fitted()
+        check_is_fitted(self, "cluster_centers_")
         arr = self._check_input(X)
         return Dataset(arr).device_engine(self._device_index()).center_distances(self.cluster_centers_)
 
     def fit_transform(self, X, y=None):
         return self.fit(X).transform(X)
-
-    def fit_predict(self, X, y=None):
-        return self.fit(X).labels_

@@ -104,3 +104,28 @@ def test_generator_matches_golden_bytes():
     g = golden("synth_10k_5_4")
     x = generate_synthetic_array(10_000, 5, 4, seed=0, dtype=np.float32)
     assert np.array_equal(x, g["coords"])
+
+
+def test_estimator_is_a_sklearn_estimator():
+    """RegimeKMeans(ClusterMixin, BaseEstimator) as the reference's (estimator.py:19): clone /
+    get_params / set_params by constructor introspection, NotFittedError before fit
+    (check_is_fitted, estimator.py:177,185) — no device needed for any of these."""
+    from sklearn.base import BaseEstimator, ClusterMixin, clone
+    from sklearn.exceptions import NotFittedError
+
+    from paper_1402_3788_b200 import RegimeKMeans
+
+    est = RegimeKMeans(5, max_iter=7, tol=1e-3, diameter_pair_cap=100)
+    assert isinstance(est, BaseEstimator) and isinstance(est, ClusterMixin)
+    p = est.get_params()
+    assert p["n_clusters"] == 5 and p["max_iter"] == 7 and p["tol"] == 1e-3 and p["diameter_pair_cap"] == 100
+    c = clone(est)
+    assert c is not est and c.get_params() == p
+    c.set_params(n_clusters=3)
+    assert c.n_clusters == 3 and est.n_clusters == 5
+    import numpy as np
+
+    with pytest.raises(NotFittedError):
+        est.predict(np.zeros((3, 2)))
+    with pytest.raises(NotFittedError):
+        est.transform(np.zeros((3, 2)))
