@@ -1064,27 +1064,26 @@ int km_converged(km_engine* e, const double* prev, const double* next, int32_t k
 static int launch_sums(km_engine* e, unsigned long long* out) {
   if (e->point_bytes != 4 || e->m > 31) return set_err(e, KM_ERR_INTERNAL, "cluster-sums kernel: fp32, m <= 31 only");
   const size_t per = (size_t)e->k * (e->m + 1) * 8;
-  const bool priv = per * (kSumsThreads / 32) <= 32 * 1024;
-  const size_t smem = priv ? per * (kSumsThreads / 32) : per;
+  const bool priv = per * kSumsWarps <= 100 * 1024;  // warp-private accumulators (2 CTAs / SM) where they fit
+  const size_t smem = sums_smem_bytes(e->m, e->k, priv);
   if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
-  auto kern = priv ? cluster_sums_f32_kernel<true> : cluster_sums_f32_kernel<false>;
+  const bool use_d = e->frac_bits > 120 || e->frac_bits < -120;
+  auto kern = priv ? (use_d ? cluster_sums_f32_kernel<true, true> : cluster_sums_f32_kernel<true, false>)
+                   : (use_d ? cluster_sums_f32_kernel<false, true> : cluster_sums_f32_kernel<false, false>);
   // launch geometry per (k, m) shape, computed once (no attribute / occupancy queries per call)
-  if (e->sums_key != per) {
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t key = smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0);
+  if (e->sums_key != key) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSumsThreads, smem));
     e->sums_per_sm = std::max(1, per_sm);
-    e->sums_key = per;
+    e->sums_key = key;
   }
-  const int per_sm = e->sums_per_sm;
-  const int64_t warps_needed = (e->n + kSumsRows * 4 - 1) / (kSumsRows * 4);  // ≥ 4 batches per warp
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)per_sm * e->num_sms,
-                                                              (warps_needed + 7) / 8));
-  CK(cudaMemsetAsync(e->recheck_count, 0, 4, e->stream));
+  const int64_t ntiles = (e->n + kSumsTile - 1) / kSumsTile;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sums_per_sm * e->num_sms, ntiles));
   kern<<<(unsigned)grid, kSumsThreads, smem, e->stream>>>((const float*)e->x, e->labels, e->n, e->m, e->k,
                                                           (float)std::ldexp(1.0, e->frac_bits),
-                                                          std::ldexp(1.0, e->frac_bits),
-                                                          (e->frac_bits > 120 || e->frac_bits < -120) ? 1 : 0, out);
+                                                          std::ldexp(1.0, e->frac_bits), out);
   CK_LAUNCH("cluster_sums_f32_kernel");
   e->stats.kernel_launches += 1;
   return KM_OK;

@@ -11,68 +11,127 @@
 // conversion the tensor-core pass uses for its per-point deltas (to_fixed) — so the running
 // totals S(L_t) = S(L0) + Σ Δ stay bit-identical to a from-scratch recomputation, for any grid.
 //
-// Layout: lane f of a warp owns feature f of every row it reads (lane m counts); the row's label
-// is warp-uniform, so one warp instruction adds a whole row into accumulator row `label` with
-// distinct addresses per lane.  PRIV: every warp owns a private [k][m+1] int64 accumulator in
-// shared memory (plain LDS/IADD/STS, no atomics); otherwise (large k·m) the CTA shares one copy
-// updated with 32-bit atomic pairs.  Rows are read 8 at a time per warp (8 independent loads per
-// lane in flight), each warp a contiguous row range (sequential DRAM pages).
+// Streaming: each CTA owns a contiguous range of 128-row tiles; one elected thread keeps a ring
+// of bulk copies (cp.async.bulk, the rows and their labels, L2 evict-first) in flight, so the
+// loads need no registers and are fully coalesced.  Consumption: lane f of a warp owns feature f
+// (lane m counts); a row's label is warp-uniform, so one warp instruction adds a whole row into
+// accumulator row `label` with distinct addresses per lane.  PRIV: every warp owns a private
+// [k][m+1] int64 accumulator (plain LDS/IADD/STS); otherwise (large k·m) the CTA shares one copy
+// updated with 32-bit atomic pairs.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include "kmeans_kernels.cuh"
+#include "kmeans_tc.cuh"
 
 namespace km {
 
-constexpr int kSumsThreads = 256;
-constexpr int kSumsRows = 8;  // rows per warp batch
+constexpr int kSumsThreads = 512;
+constexpr int kSumsWarps = kSumsThreads / 32;
+constexpr int kSumsTile = 128;                      // rows per bulk tile (kSumsWarps × 8)
+constexpr int kSumsStages = 4;                      // tiles in flight per CTA
 
-template <bool PRIV>
+// shared memory: [stages] × (row tile + labels) ring, then the accumulators
+__host__ __device__ inline size_t sums_stage_bytes(int m) {
+  return (((size_t)kSumsTile * m * 4 + 15) & ~(size_t)15) + kSumsTile * 4;
+}
+__host__ __device__ inline size_t sums_smem_bytes(int m, int k, bool priv) {
+  return 1024 + kSumsStages * sums_stage_bytes(m) + (size_t)(priv ? kSumsWarps : 1) * k * (m + 1) * 8;
+}
+
+// One tile's rows of this warp into its accumulator (lane f ≤ m; lane m counts).
+template <bool PRIV, bool USE_D>
+__device__ __forceinline__ void sums_rows(const float* __restrict__ sx, const int32_t* __restrict__ sl, int r0, int r1,
+                                          int m, int lane, unsigned long long* acc, int row_len, float scale_f,
+                                          double scale_d) {
+#pragma unroll 4
+  for (int r = r0; r < r1; ++r) {
+    const int L = sl[r];                                      // warp-uniform (broadcast)
+    unsigned long long q = 1ull;                              // lane m: the count
+    if (lane < m) {
+      const float v = sx[r * m + lane];
+      q = (unsigned long long)(USE_D ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f)));
+    }
+    unsigned long long* dst = acc + L * row_len + lane;
+    if (PRIV) *dst += q; else smem_add64(dst, q);
+  }
+}
+
+template <bool PRIV, bool USE_D>
 __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
     const float* __restrict__ x, const int32_t* __restrict__ labels, int64_t n, int m, int k, float scale_f,
-    double scale_d, int use_dscale, unsigned long long* __restrict__ out /* [k·m sums][k counts] */) {
-  extern __shared__ unsigned long long s_acc[];
+    double scale_d, unsigned long long* __restrict__ out /* [k·m sums][k counts] */) {
+  extern __shared__ __align__(1024) unsigned char s_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_raw);      // [stages]
+  uint64_t* empty = full + kSumsStages;                      // [stages]
+  unsigned char* ring = s_raw + 1024;
+  const size_t stage = sums_stage_bytes(m);
+  const size_t xbytes_max = stage - kSumsTile * 4;
+  unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(ring + kSumsStages * stage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int W = kSumsThreads / 32;
-  const int row_len = m + 1;
-  const int per = k * row_len;
-  const int copies = PRIV ? W : 1;
+  const int row_len = m + 1, per = k * row_len, copies = PRIV ? kSumsWarps : 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSumsStages; ++s) {
+      tc::mbar_init(full + s, 1);
+      tc::mbar_init(empty + s, kSumsWarps);
+    }
+    tc::fence_barrier_init();
+  }
   for (int i = threadIdx.x; i < per * copies; i += kSumsThreads) s_acc[i] = 0ull;
   __syncthreads();
   unsigned long long* acc = s_acc + (PRIV ? (size_t)warp * per : 0);
 
-  const int64_t gw = (int64_t)blockIdx.x * W + warp, nw = (int64_t)gridDim.x * W;
-  const int64_t r_lo = n * gw / nw, r_hi = n * (gw + 1) / nw;
-  const bool feat = lane < m, cnt_lane = lane == m;
-  for (int64_t r = r_lo; r < r_hi; r += kSumsRows) {
-    const int rows = (int)(r_hi - r < (int64_t)kSumsRows ? r_hi - r : (int64_t)kSumsRows);
-    const int lab = lane < rows ? __ldg(labels + r + lane) : 0;
-    float v[kSumsRows];
-#pragma unroll
-    for (int j = 0; j < kSumsRows; ++j) v[j] = (feat && j < rows) ? __ldg(x + (r + j) * m + lane) : 0.f;
-#pragma unroll
-    for (int j = 0; j < kSumsRows; ++j) {
-      const int L = __shfl_sync(0xffffffffu, lab, j);
-      if (j < rows && (unsigned)L < (unsigned)k) {
-        unsigned long long* dst = acc + (size_t)L * row_len + lane;
-        if (feat) {
-          const unsigned long long q = (unsigned long long)to_fixed<float>(v[j], scale_f, scale_d, use_dscale);
-          if (PRIV) *dst += q; else smem_add64(dst, q);
-        } else if (cnt_lane) {
-          if (PRIV) *dst += 1ull; else smem_add64(dst, 1ull);
-        }
-      }
+  const int64_t ntiles = (n + kSumsTile - 1) / kSumsTile;
+  const int64_t t_lo = ntiles * blockIdx.x / gridDim.x, t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
+  const int my = (int)(t_hi - t_lo);
+  // the last tile of the array may be ragged: its tail (≤ 3 floats / labels past the 16-byte
+  // bulk granule) is patched in from global memory by the CTA that owns it
+  auto issue = [&](int i) {  // tile i of this CTA → stage i % S (one thread)
+    const int s = i % kSumsStages;
+    if (i >= kSumsStages) tc::mbar_wait(empty + s, ((i / kSumsStages) - 1) & 1);
+    const int64_t row0 = (t_lo + i) * kSumsTile;
+    const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
+    const uint32_t xb = ((uint32_t)rows * m * 4u) & ~15u, lb = ((uint32_t)rows * 4u) & ~15u;
+    tc::mbar_arrive_expect_tx(full + s, xb + lb);
+    unsigned char* dst = ring + s * stage;
+    const uint64_t pol = tc::l2_policy_evict_first();
+    if (xb) tc::bulk_g2s_hint(dst, x + row0 * m, xb, full + s, pol);
+    if (lb) tc::bulk_g2s_hint(dst + xbytes_max, labels + row0, lb, full + s, pol);
+  };
+  if (threadIdx.x == 0)
+    for (int i = 0; i < min(my, kSumsStages); ++i) issue(i);
+
+  constexpr int RPW = kSumsTile / kSumsWarps;  // rows per warp and tile
+  const bool active = lane <= m;
+  for (int i = 0; i < my; ++i) {
+    const int s = i % kSumsStages;
+    const int64_t row0 = (t_lo + i) * kSumsTile;
+    const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
+    tc::mbar_wait(full + s, (i / kSumsStages) & 1);
+    float* sx = reinterpret_cast<float*>(ring + s * stage);
+    int32_t* sl = reinterpret_cast<int32_t*>(ring + s * stage + xbytes_max);
+    if (rows < kSumsTile) {  // ragged last tile: patch the sub-granule tail from global memory
+      const uint32_t xe = (((uint32_t)rows * m * 4u) & ~15u) / 4u, le = (((uint32_t)rows * 4u) & ~15u) / 4u;
+      __syncthreads();  // (only the CTA owning the last tile gets here; every warp takes this branch)
+      for (uint32_t e = xe + threadIdx.x; e < (uint32_t)rows * m; e += kSumsThreads) sx[e] = __ldg(x + row0 * m + e);
+      for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsThreads) sl[e] = __ldg(labels + row0 + e);
+      __syncthreads();
     }
+    const int r0 = min(warp * RPW, rows), r1 = min(r0 + RPW, rows);
+    if (active) sums_rows<PRIV, USE_D>(sx, sl, r0, r1, m, lane, acc, row_len, scale_f, scale_d);
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(empty + s);
+    if (threadIdx.x == 0 && i + kSumsStages < my) issue(i + kSumsStages);
   }
   __syncthreads();
   // one global atomic per non-zero accumulator and CTA
   for (int i = threadIdx.x; i < per; i += kSumsThreads) {
-    unsigned long long s = 0;
-    for (int w = 0; w < copies; ++w) s += s_acc[(size_t)w * per + i];
-    if (s) {
+    unsigned long long v = 0;
+    for (int w = 0; w < copies; ++w) v += s_acc[(size_t)w * per + i];
+    if (v) {
       const int c = i / row_len, f = i - c * row_len;
-      atomicAdd(out + (f < m ? (size_t)c * m + f : (size_t)k * m + c), s);
+      atomicAdd(out + (f < m ? (size_t)c * m + f : (size_t)k * m + c), v);
     }
   }
 }

@@ -105,3 +105,54 @@ class FakeStepEngine:
 
     def step_read(self, k, want_labels=True):
         return self.cur.copy(), self.model_counts.copy(), (self.labels.copy() if want_labels else None)
+
+
+class FakeLoopEngine(FakeStepEngine):
+    """The device-state loop API on top of the step API (km_step_loop_* in include/kmeans_b200.h):
+    the loop state lives "on the device" (here: in this object, mirroring DevState), passes and
+    finishes are GATED on it — once the loop is done or waits for the host (empty clusters) they do
+    no work and leave the partial buffer zero, exactly as the CUDA kernels do — so
+    distributed._run_batched can enqueue several [allreduce, finish, pass] iterations per host
+    round trip.  Same rules as lloyd_finish_kernel / lloyd_check_kernel (kmeans_finish.cuh):
+    update + empties + congruence + exhaustion, and the exhausted run's final assign is folded
+    into the counts (engine.py:339-343)."""
+
+    def loop_begin(self, max_iters, tol):
+        self.st = dict(t=0, done=0, converged=0, exhausted=0, need_host=0, max_iters=int(max_iters), tol=float(tol))
+        self.gated_passes = 0
+
+    def loop_pass(self):
+        if self.st["done"] or self.st["need_host"]:
+            self.gated_passes += 1
+            return  # gated: the partial buffer stays zero (the allreduce then sums zeros)
+        self.step_pass()
+
+    def loop_finish(self):
+        st = self.st
+        if st["done"] or st["need_host"]:
+            self.part.zero_()
+            return
+        if st["exhausted"]:  # the final assign pass of an exhausted run: counts = bincount(L_T)
+            self.step_fold()
+            st["done"] = 1
+            return
+        n_empty, conv = self.step_finish(st["tol"])
+        st["t"] += 1
+        if n_empty:
+            st["need_host"] = 1
+        elif conv:
+            st["converged"] = st["done"] = 1
+        elif st["t"] >= st["max_iters"]:
+            st["exhausted"] = 1
+
+    def loop_check(self):
+        st = self.st
+        st["need_host"] = 0
+        if oracle.converged(self.prev, self.cur, st["tol"]):
+            st["converged"] = st["done"] = 1
+        elif st["t"] >= st["max_iters"]:
+            st["exhausted"] = 1
+
+    def loop_state(self):
+        st = self.st
+        return st["t"], bool(st["done"]), bool(st["converged"]), bool(st["need_host"])

@@ -28,74 +28,59 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, x, c0, max_iters, tol, outdir):
+def _worker(rank, world, port, cases, outdir):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     import torch.distributed as dist
 
-    from fake_step_engine import FakeStepEngine
+    from fake_step_engine import FakeLoopEngine, FakeStepEngine
     from paper_1402_3788_b200.distributed import TorchCollective, run_sharded, shard_rows
 
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    lo, hi = shard_rows(x.shape[0], world, rank)
-    eng = FakeStepEngine(x[lo:hi])
-    res = run_sharded(eng, TorchCollective(), c0, max_iters=max_iters, tol=tol)
-    np.savez(Path(outdir) / f"rank{rank}.npz", centers=res.centers, counts=res.counts, labels=res.labels,
-             iterations=res.iterations, converged=res.converged, row_offset=res.row_offset, lo=lo)
+    for i, (x, c0, max_iters, tol, batched) in enumerate(cases):  # several cases per spawn (start-up cost)
+        lo, hi = shard_rows(x.shape[0], world, rank)
+        eng = (FakeLoopEngine if batched else FakeStepEngine)(x[lo:hi])
+        res = run_sharded(eng, TorchCollective(), c0, max_iters=max_iters, tol=tol)
+        assert not batched or hasattr(eng, "st"), "the batched device-state loop must have run"
+        np.savez(Path(outdir) / f"case{i}_rank{rank}.npz", centers=res.centers, counts=res.counts, labels=res.labels,
+                 iterations=res.iterations, converged=res.converged, row_offset=res.row_offset, lo=lo)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def run_world(world, x, c0, max_iters=1000, tol=0.0):
+def run_world(world, cases):
+    """cases: [(x, c0, max_iters, tol, batched)] → [(rank-0 result, gathered labels)]"""
+    out = []
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_worker, args=(world, _free_port(), x, c0, max_iters, tol, d), nprocs=world, join=True)
-        parts = [dict(np.load(Path(d) / f"rank{r}.npz")) for r in range(world)]
-    for r, p in enumerate(parts):
-        assert int(p["row_offset"]) == int(p["lo"])
-        assert np.array_equal(p["centers"], parts[0]["centers"]), "centres must be replicated bit-identically"
-        assert np.array_equal(p["counts"], parts[0]["counts"])
-        assert int(p["iterations"]) == int(parts[0]["iterations"])
-    labels = np.concatenate([p["labels"] for p in parts])
-    return parts[0], labels
+        mp.spawn(_worker, args=(world, _free_port(), cases, d), nprocs=world, join=True)
+        for i in range(len(cases)):
+            parts = [dict(np.load(Path(d) / f"case{i}_rank{r}.npz")) for r in range(world)]
+            for p in parts:
+                assert int(p["row_offset"]) == int(p["lo"])
+                assert np.array_equal(p["centers"], parts[0]["centers"]), "centres must be replicated bit-identically"
+                assert np.array_equal(p["counts"], parts[0]["counts"])
+                assert int(p["iterations"]) == int(parts[0]["iterations"])
+            out.append((parts[0], np.concatenate([p["labels"] for p in parts])))
+    return out
 
 
-def _check(x, c0, world, max_iters=1000, tol=0.0):
+def _check_many(world, cases):
     from oracle import oracle
 
-    want = oracle.lloyd(x, c0, max_iters=max_iters, tol=tol)
-    got, labels = run_world(world, x, c0, max_iters, tol)
-    assert int(got["iterations"]) == want["iterations"]
-    assert bool(got["converged"]) == want["converged"]
-    assert np.array_equal(labels, want["labels"])
-    assert np.array_equal(got["counts"], want["counts"])
-    rel = np.max(np.abs(got["centers"] - want["centers"]) / np.maximum(np.abs(want["centers"]), 1.0))
-    assert rel <= 1e-12, rel
+    for (x, c0, max_iters, tol, _), (got, labels) in zip(cases, run_world(world, cases)):
+        want = oracle.lloyd(x, c0, max_iters=max_iters, tol=tol)
+        assert int(got["iterations"]) == want["iterations"]
+        assert bool(got["converged"]) == want["converged"]
+        assert np.array_equal(labels, want["labels"])
+        assert np.array_equal(got["counts"], want["counts"])
+        rel = np.max(np.abs(got["centers"] - want["centers"]) / np.maximum(np.abs(want["centers"]), 1.0))
+        assert rel <= 1e-12, rel
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_sharded_matches_single_process(world):
-    from paper_1402_3788_b200.datasets import generate_synthetic_array
-
-    x = generate_synthetic_array(3001, 5, 4, seed=3, dtype=np.float32).astype(np.float64)
-    _check(x, x[:4].copy(), world)
-
-
-def test_sharded_exhausted_run():
-    from paper_1402_3788_b200.datasets import generate_synthetic_array
-
-    x = generate_synthetic_array(2000, 6, 5, seed=8, dtype=np.float32).astype(np.float64)
-    _check(x, x[:5].copy(), 2, max_iters=3)
-
-
-def test_sharded_empty_cluster_repair_across_shards():
-    # duplicated initial centres: the duplicates start empty and are re-seeded by the
-    # global (max d², lowest row) rule across both shards
-    from conftest import golden
-
-    g = golden("all_dup_repair")
-    _check(g["coords"].astype(np.float64), g["c0"], 2)
+def _check(x, c0, world, max_iters=1000, tol=0.0, batched=False):
+    _check_many(world, [(x, c0, max_iters, tol, batched)])
 
 
 def test_shard_rows_rule():
@@ -105,3 +90,29 @@ def test_shard_rows_rule():
     spans = [shard_rows(1001, 8, r) for r in range(8)]
     assert spans[0][0] == 0 and spans[-1][1] == 1001
     assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+# --- the batched device-state loop (distributed._run_batched: several [allreduce, finish, pass]
+# iterations per host round trip, gated kernels) — the branch the NCCL/GPU path takes -------------
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_matches_single_process(world):
+    """Both host loops of distributed.run_sharded — the per-iteration step loop and the batched
+    device-state loop (_run_batched: several [allreduce, finish, pass] iterations per host round
+    trip, gated kernels; the branch the NCCL/GPU path takes) — on converged runs, exhausted runs
+    (max_iters 1 / 3 / 17: the final assign folded into the counts) and empty clusters (duplicated
+    initial centres; the batched loop stops mid-batch, the host runs the global repair — argmax
+    across shards — the check and the repaired assignment, then batching resumes)."""
+    from conftest import golden
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(3001, 5, 4, seed=3, dtype=np.float32).astype(np.float64)
+    y = generate_synthetic_array(2000, 6, 5, seed=8, dtype=np.float32).astype(np.float64)
+    g1, g2 = golden("all_dup_repair"), golden("dup_center_repair")
+    cases = []
+    for batched in (False, True):
+        cases += [(x, x[:4].copy(), 1000, 0.0, batched)]
+        cases += [(y, y[:5].copy(), it, 0.0, batched) for it in (1, 3, 17)]
+        cases += [(g["coords"].astype(np.float64), g["c0"], 1000, 0.0, batched) for g in (g1, g2)]
+    _check_many(world, cases)
