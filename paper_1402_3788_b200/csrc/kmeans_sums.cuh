@@ -27,8 +27,8 @@
 
 namespace km {
 
-constexpr int kSumsThreads = 512;
-constexpr int kSumsWarps = kSumsThreads / 32;
+constexpr int kSumsWarps = 16;                      // consumer warps (+ one producer warp)
+constexpr int kSumsThreads = (kSumsWarps + 1) * 32;
 constexpr int kSumsTile = 128;                      // rows per bulk tile (kSumsWarps × 8)
 constexpr int kSumsStages = 4;                      // tiles in flight per CTA
 
@@ -99,30 +99,32 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
     if (xb) tc::bulk_g2s_hint(dst, x + row0 * m, xb, full + s, pol);
     if (lb) tc::bulk_g2s_hint(dst + xbytes_max, labels + row0, lb, full + s, pol);
   };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < min(my, kSumsStages); ++i) issue(i);
-
   constexpr int RPW = kSumsTile / kSumsWarps;  // rows per warp and tile
-  const bool active = lane <= m;
-  for (int i = 0; i < my; ++i) {
-    const int s = i % kSumsStages;
-    const int64_t row0 = (t_lo + i) * kSumsTile;
-    const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
-    tc::mbar_wait(full + s, (i / kSumsStages) & 1);
-    float* sx = reinterpret_cast<float*>(ring + s * stage);
-    int32_t* sl = reinterpret_cast<int32_t*>(ring + s * stage + xbytes_max);
-    if (rows < kSumsTile) {  // ragged last tile: patch the sub-granule tail from global memory
-      const uint32_t xe = (((uint32_t)rows * m * 4u) & ~15u) / 4u, le = (((uint32_t)rows * 4u) & ~15u) / 4u;
-      __syncthreads();  // (only the CTA owning the last tile gets here; every warp takes this branch)
-      for (uint32_t e = xe + threadIdx.x; e < (uint32_t)rows * m; e += kSumsThreads) sx[e] = __ldg(x + row0 * m + e);
-      for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsThreads) sl[e] = __ldg(labels + row0 + e);
-      __syncthreads();
+  if (warp == kSumsWarps) {  // producer warp: one thread keeps the ring full
+    if (lane == 0)
+      for (int i = 0; i < my; ++i) issue(i);
+  } else {
+    const bool active = lane <= m;
+    for (int i = 0; i < my; ++i) {
+      const int s = i % kSumsStages;
+      const int64_t row0 = (t_lo + i) * kSumsTile;
+      const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
+      // one warp polls the barrier, the others park in bar.sync (no wake-up storms)
+      if (warp == 0) tc::mbar_wait(full + s, (i / kSumsStages) & 1);
+      tc::named_bar_sync(1, kSumsWarps * 32);
+      float* sx = reinterpret_cast<float*>(ring + s * stage);
+      int32_t* sl = reinterpret_cast<int32_t*>(ring + s * stage + xbytes_max);
+      if (rows < kSumsTile) {  // ragged last tile: patch the sub-granule tail from global memory
+        const uint32_t xe = (((uint32_t)rows * m * 4u) & ~15u) / 4u, le = (((uint32_t)rows * 4u) & ~15u) / 4u;
+        for (uint32_t e = xe + threadIdx.x; e < (uint32_t)rows * m; e += kSumsWarps * 32) sx[e] = __ldg(x + row0 * m + e);
+        for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsWarps * 32) sl[e] = __ldg(labels + row0 + e);
+        tc::named_bar_sync(1, kSumsWarps * 32);
+      }
+      const int r0 = min(warp * RPW, rows), r1 = min(r0 + RPW, rows);
+      if (active) sums_rows<PRIV, USE_D>(sx, sl, r0, r1, m, lane, acc, row_len, scale_f, scale_d);
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(empty + s);
     }
-    const int r0 = min(warp * RPW, rows), r1 = min(r0 + RPW, rows);
-    if (active) sums_rows<PRIV, USE_D>(sx, sl, r0, r1, m, lane, acc, row_len, scale_f, scale_d);
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(empty + s);
-    if (threadIdx.x == 0 && i + kSumsStages < my) issue(i + kSumsStages);
   }
   __syncthreads();
   // one global atomic per non-zero accumulator and CTA

@@ -189,6 +189,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait of a role that is normally ahead of its producer (the epilogue on the MMA): a failed
 // try_wait returns on any barrier event of the CTA, so with 12 epilogue warps waiting the retry
 // loop would take a quarter of the SM's issue slots away from the transform; back off instead.
+// Group waits: in each 4-warp transform / epilogue group only one warp polls the mbarrier (a
+// failed try_wait wakes on every barrier event of the CTA — with 20 waiting warps the retry loops
+// were ~25% of all issued instructions); the others park in a named barrier (bar.sync issues
+// nothing while blocked) and proceed after tcgen05.fence::after_thread_sync.
+#ifndef KM_GROUP_WAIT
+#define KM_GROUP_WAIT 1
+#endif
 #ifndef KM_EPI_SLEEP
 #define KM_EPI_SLEEP 0
 #endif
@@ -862,7 +869,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[0] = clock64();
-        mbar_wait(full_raw + s, (g / RS) & 1);
+        if (KM_GROUP_WAIT) {  // one warp of the group polls both barriers, the other three park in bar.sync
+          if ((warp & 3) == 0) {
+            mbar_wait(full_raw + s, (g / RS) & 1);
+            if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+          }
+          named_bar_sync(1 + kEpiGroups + tg, 128);
+          tc_fence_after();
+        } else {
+          mbar_wait(full_raw + s, (g / RS) & 1);
+        }
         if (stamp) ts[1] = clock64();
         if (KM_DBG_FLAGS & 4) {  // tuning only: measure the TMA stream alone
           __syncwarp();
@@ -870,7 +886,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           continue;
         }
         const float* rs = raw + s * (S.raw_stride / 4);
-        if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+        if (!KM_GROUP_WAIT && g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
         if (stamp) ts[7] = clock64();
         unsigned char* s_a = sm + S.off_a + sa * (TR * 128);
 #pragma unroll
@@ -994,7 +1010,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[4] = clock64();
-        mbar_wait_backoff(s_full + ss, (g / TM::NS) & 1);
+        if (KM_GROUP_WAIT) {  // one warp of the group polls the barrier, the other three park in bar.sync
+          if ((ew & 3) == 0) mbar_wait_backoff(s_full + ss, (g / TM::NS) & 1);
+          named_bar_sync(1 + e, 128);
+        } else {
+          mbar_wait_backoff(s_full + ss, (g / TM::NS) & 1);
+        }
         if (stamp) ts[5] = clock64();
         tc_fence_after();
         if (KM_DBG_FLAGS & 32) {  // timing experiment only: no epilogue work (labels unchanged)
