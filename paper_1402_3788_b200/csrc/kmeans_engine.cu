@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/kmeans_b200.h"
@@ -788,6 +789,45 @@ static int download_labels(km_engine* e, int64_t* out) {
   return KM_OK;
 }
 
+// Exact fixed-point sums + counts of every resident point by its current label, added into `out`
+// ([k·m sums][k counts], zeroed by the caller): one HBM stream, warp-private accumulators where
+// they fit (kmeans_sums.cuh).  Also clears the recheck overflow counter of the pass before it.
+static int launch_sums(km_engine* e, unsigned long long* out) {
+  if (e->point_bytes != 4 || e->m > 31) return set_err(e, KM_ERR_INTERNAL, "cluster-sums kernel: fp32, m <= 31 only");
+  const size_t per = (size_t)e->k * (e->m + 1) * 8;
+  const bool priv = per * kSumsWarps <= 100 * 1024;  // warp-private accumulators (2 CTAs / SM) where they fit
+  const size_t smem = sums_smem_bytes(e->m, e->k, priv);
+  if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
+  const bool use_d = e->frac_bits > 120 || e->frac_bits < -120;
+  // compile-time feature counts for the BASELINE shapes (full tiles at immediate offsets)
+  auto pick = [&](auto mt) {
+    constexpr int MT = decltype(mt)::value;
+    return priv ? (use_d ? cluster_sums_f32_kernel<MT, true, true> : cluster_sums_f32_kernel<MT, true, false>)
+                : (use_d ? cluster_sums_f32_kernel<MT, false, true> : cluster_sums_f32_kernel<MT, false, false>);
+  };
+  auto kern = e->m == 25 ? pick(std::integral_constant<int, 25>{})
+              : e->m == 10 ? pick(std::integral_constant<int, 10>{})
+              : e->m == 5 ? pick(std::integral_constant<int, 5>{})
+                          : pick(std::integral_constant<int, 0>{});
+  // launch geometry per (k, m) shape, computed once (no attribute / occupancy queries per call)
+  const size_t key = (smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0)) * 64 + (size_t)e->m;
+  if (e->sums_key != key) {
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSumsThreads, smem));
+    e->sums_per_sm = std::max(1, per_sm);
+    e->sums_key = key;
+  }
+  const int64_t ntiles = (e->n + kSumsTile - 1) / kSumsTile;
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sums_per_sm * e->num_sms, ntiles));
+  kern<<<(unsigned)grid, kSumsThreads, smem, e->stream>>>((const float*)e->x, e->labels, e->n, e->m, e->k,
+                                                          (float)std::ldexp(1.0, e->frac_bits),
+                                                          std::ldexp(1.0, e->frac_bits), out);
+  CK_LAUNCH("cluster_sums_f32_kernel");
+  e->stats.kernel_launches += 1;
+  return KM_OK;
+}
+
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
@@ -1016,7 +1056,13 @@ int km_update(km_engine* e, int64_t* labels_inout, int32_t k, double* centers_ou
   CK(cudaMemcpyAsync(e->labels, lab.data(), 4 * (size_t)e->n, cudaMemcpyHostToDevice, e->stream));
   if ((r = reset_state(e, 1, 0.0))) return r;
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
-  if ((r = launch_pass(e, PASS_SUMS_ONLY, false))) return r;
+  // labels were validated on the host: fp32 points with m ≤ 31 take the streaming cluster-sums
+  // kernel (kmeans_sums.cuh), other shapes the SIMT pass in sums-only mode
+  if (e->point_bytes == 4 && e->m <= 31) {
+    if ((r = launch_sums(e, e->part))) return r;
+  } else if ((r = launch_pass(e, PASS_SUMS_ONLY, false))) {
+    return r;
+  }
   if ((r = launch_finish(e, 1, false))) return r;
   e->next_full = true;
   if ((r = read_state(e))) return r;
@@ -1055,37 +1101,6 @@ int km_converged(km_engine* e, const double* prev, const double* next, int32_t k
   cudaFree(buf);
   if (c != cudaSuccess) return cuda_fail(e, c, "km_converged");
   *out = h;
-  return KM_OK;
-}
-
-// Exact fixed-point sums + counts of every resident point by its current label, added into `out`
-// ([k·m sums][k counts], zeroed by the caller): one HBM stream, warp-private accumulators where
-// they fit (kmeans_sums.cuh).  Also clears the recheck overflow counter of the pass before it.
-static int launch_sums(km_engine* e, unsigned long long* out) {
-  if (e->point_bytes != 4 || e->m > 31) return set_err(e, KM_ERR_INTERNAL, "cluster-sums kernel: fp32, m <= 31 only");
-  const size_t per = (size_t)e->k * (e->m + 1) * 8;
-  const bool priv = per * kSumsWarps <= 100 * 1024;  // warp-private accumulators (2 CTAs / SM) where they fit
-  const size_t smem = sums_smem_bytes(e->m, e->k, priv);
-  if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
-  const bool use_d = e->frac_bits > 120 || e->frac_bits < -120;
-  auto kern = priv ? (use_d ? cluster_sums_f32_kernel<true, true> : cluster_sums_f32_kernel<true, false>)
-                   : (use_d ? cluster_sums_f32_kernel<false, true> : cluster_sums_f32_kernel<false, false>);
-  // launch geometry per (k, m) shape, computed once (no attribute / occupancy queries per call)
-  const size_t key = smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0);
-  if (e->sums_key != key) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSumsThreads, smem));
-    e->sums_per_sm = std::max(1, per_sm);
-    e->sums_key = key;
-  }
-  const int64_t ntiles = (e->n + kSumsTile - 1) / kSumsTile;
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sums_per_sm * e->num_sms, ntiles));
-  kern<<<(unsigned)grid, kSumsThreads, smem, e->stream>>>((const float*)e->x, e->labels, e->n, e->m, e->k,
-                                                          (float)std::ldexp(1.0, e->frac_bits),
-                                                          std::ldexp(1.0, e->frac_bits), out);
-  CK_LAUNCH("cluster_sums_f32_kernel");
-  e->stats.kernel_launches += 1;
   return KM_OK;
 }
 

@@ -58,7 +58,25 @@ __device__ __forceinline__ void sums_rows(const float* __restrict__ sx, const in
   }
 }
 
-template <bool PRIV, bool USE_D>
+// Full 128-row tile, compile-time m (MT): the warp's RPW rows at immediate offsets.  The count
+// lane (lane MT) converts cnt_v = 2^-F, which the fixed-point conversion maps to exactly 1, so
+// every lane runs the same instruction stream: ~10 warp instructions per row.
+template <int MT, int RPW, bool PRIV>
+__device__ __forceinline__ void sums_rows_full(const float* __restrict__ sxw, const int32_t* __restrict__ slw,
+                                               int lane, unsigned long long* acc_lane, float scale_f, float cnt_v) {
+  const bool feat = lane < MT;
+#pragma unroll
+  for (int j = 0; j < RPW; ++j) {
+    const int L = slw[j];
+    const float v = feat ? sxw[j * MT] : cnt_v;
+    const unsigned long long q = (unsigned long long)__float2ll_rn(__fmul_rn(v, scale_f));
+    unsigned long long* dst = acc_lane + L * (MT + 1);
+    if (PRIV) *dst += q; else smem_add64(dst, q);
+  }
+}
+
+// MT > 0: compile-time feature count (the full-tile fast path); MT = 0: runtime m
+template <int MT, bool PRIV, bool USE_D>
 __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
     const float* __restrict__ x, const int32_t* __restrict__ labels, int64_t n, int m, int k, float scale_f,
     double scale_d, unsigned long long* __restrict__ out /* [k·m sums][k counts] */) {
@@ -100,6 +118,7 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
     if (lb) tc::bulk_g2s_hint(dst + xbytes_max, labels + row0, lb, full + s, pol);
   };
   constexpr int RPW = kSumsTile / kSumsWarps;  // rows per warp and tile
+  const float cnt_v = 1.0f / scale_f;          // = 2^-F: converts to exactly 1 (the count lane)
   if (warp == kSumsWarps) {  // producer warp: one thread keeps the ring full
     if (lane == 0)
       for (int i = 0; i < my; ++i) issue(i);
@@ -120,8 +139,14 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
         for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsWarps * 32) sl[e] = __ldg(labels + row0 + e);
         tc::named_bar_sync(1, kSumsWarps * 32);
       }
-      const int r0 = min(warp * RPW, rows), r1 = min(r0 + RPW, rows);
-      if (active) sums_rows<PRIV, USE_D>(sx, sl, r0, r1, m, lane, acc, row_len, scale_f, scale_d);
+      if (MT > 0 && !USE_D && rows == kSumsTile) {
+        if (active)
+          sums_rows_full<(MT > 0 ? MT : 1), RPW, PRIV>(sx + warp * RPW * MT + (lane < m ? lane : 0), sl + warp * RPW, lane,
+                                                       acc + lane, scale_f, cnt_v);
+      } else {
+        const int r0 = min(warp * RPW, rows), r1 = min(r0 + RPW, rows);
+        if (active) sums_rows<PRIV, USE_D>(sx, sl, r0, r1, m, lane, acc, row_len, scale_f, scale_d);
+      }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(empty + s);
     }

@@ -189,12 +189,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait of a role that is normally ahead of its producer (the epilogue on the MMA): a failed
 // try_wait returns on any barrier event of the CTA, so with 12 epilogue warps waiting the retry
 // loop would take a quarter of the SM's issue slots away from the transform; back off instead.
-// Group waits: in each 4-warp transform / epilogue group only one warp polls the mbarrier (a
+// Group waits (tuning knob, off: measured slower — 44.6 vs 43.6 µs per steady pass, the bar.sync
+// hand-off adds latency): in each 4-warp transform / epilogue group only one warp polls the mbarrier (a
 // failed try_wait wakes on every barrier event of the CTA — with 20 waiting warps the retry loops
 // were ~25% of all issued instructions); the others park in a named barrier (bar.sync issues
 // nothing while blocked) and proceed after tcgen05.fence::after_thread_sync.
 #ifndef KM_GROUP_WAIT
-#define KM_GROUP_WAIT 1
+#define KM_GROUP_WAIT 0
 #endif
 #ifndef KM_EPI_SLEEP
 #define KM_EPI_SLEEP 0

@@ -129,3 +129,14 @@ def test_estimator_is_a_sklearn_estimator():
         est.predict(np.zeros((3, 2)))
     with pytest.raises(NotFittedError):
         est.transform(np.zeros((3, 2)))
+
+
+@pytest.mark.parametrize("n,m,k,lo,hi", [(10007, 5, 4, 0, 10007), (10007, 5, 4, 123, 5000), (50000, 25, 16, 25000, 50000),
+                                         (3000, 3, 7, 2999, 3000), (3000, 3, 7, 10, 10)])
+def test_synthetic_shard_is_a_slice_of_the_full_dataset(n, m, k, lo, hi):
+    """bench.py's row shards of ONE dataset (the 64M strong-scaling config) are the same bytes as
+    rows [lo, hi) of the reference generator's array (datasets.py:73-97)."""
+    from paper_1402_3788_b200.datasets import generate_synthetic_shard
+
+    full = generate_synthetic_array(n, m, k, seed=0, dtype=np.float32)
+    assert np.array_equal(generate_synthetic_shard(n, m, k, 0, lo, hi, chunk_rows=777), full[lo:hi])
