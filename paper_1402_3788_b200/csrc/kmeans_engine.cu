@@ -1814,6 +1814,7 @@ int km_debug_filter_scores(km_engine* e, const double* centers, int32_t k, float
   if ((r = check_centers(e, centers, k))) return r;
   if ((r = ensure_k(e, k))) return r;
   if (!use_tc(e)) return set_err(e, KM_ERR_CAPACITY, "tensor-core filter not available for this shape");
+  scale_for_centers(e, centers, k);
   float* dbg = nullptr;
   if ((r = dalloc(e, &dbg, sizeof(float) * (size_t)e->n * k))) return r;
   CK(cudaMemcpyAsync(e->cur, centers, 8 * (size_t)k * e->m, cudaMemcpyHostToDevice, e->stream));

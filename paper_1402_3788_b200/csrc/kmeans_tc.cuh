@@ -46,6 +46,12 @@ namespace tc {
 
 constexpr int kQueueCap = 768;                     // per-CTA staging of uncertified points (smem)
 constexpr long long kQueueFlag = 1ll << 62;
+// a queue entry of a point whose label CHANGED (not a recheck): flag | change | row << 16 |
+// (old + 1) << 8 | new.  The recheck warp applies its exact Δ off the epilogue's critical path.
+constexpr long long kChangeFlag = 1ll << 61;
+#ifndef KM_QUEUE_CHANGES
+#define KM_QUEUE_CHANGES 1
+#endif
 constexpr int kTileRows = 128;
 #ifndef KM_TRANSFORM_GROUPS
 #define KM_TRANSFORM_GROUPS 2
@@ -732,7 +738,30 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (pst && it < 256 && blockIdx.x == 0) pst[it * 8 + 0] = globaltimer();
     if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2] = (long long)globaltimer();
     // exact re-decision of queue entry q (thread per point, candidate centres only); Δ into s_acc
+    // Δ of a changed point (queued by the epilogue): its row from global memory (L2: streamed
+    // moments ago), + to the new cluster, − from the old one
+    auto apply_change = [&](unsigned int q, long long ent) {
+      const long long row = (ent >> 16) & ((1ll << 44) - 1);
+      const int old = (int)((ent >> 8) & 0xff) - 1, nw = (int)(ent & 0xff);
+      const float* xr = a.x + row * m;
+      float xq[MP];
+#pragma unroll
+      for (int f = 0; f < MP; ++f) xq[f] = (f < m) ? __ldg(xr + f) : 0.f;
+#pragma unroll
+      for (int f = 0; f < MP; ++f) {
+        if (f < m) {
+          const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
+                                           : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
+          smem_add64(s_acc + (size_t)nw * m + f, (unsigned long long)v);
+          if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
+        }
+      }
+      smem_add64(s_acc + (size_t)km + nw, 1ull);
+      if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+      s_q[q] = 0;  // free for the next pass
+    };
     auto redecide = [&](unsigned int q, long long ent) {
+      if (ent & kChangeFlag) { apply_change(q, ent); return; }
       const long long row = (ent >> 8) & ((1ll << 54) - 1);
       const int old = (int)(ent & 0xff) - 1;
       uint32_t mk[MW];
@@ -1129,10 +1158,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         for (int mb = 0; mb < MB; ++mb) {
           const int bi = bis[mb], old = olds[mb];
           // --- exact incremental update of the per-cluster fixed-point sums (delta_rows)
-          const bool chg = bi != old;
+          bool chg = bi != old;
           if (chg) {
             ++my_changed;
             a.labels[row0 + 128 * mb + p] = bi;
+          }
+          if (KM_QUEUE_CHANGES && !full && chg && !no_sums) {
+            // hand the Δ to the recheck warp (its loads and atomics leave the epilogue's critical
+            // path); a full queue (rare) keeps it here
+            const unsigned int slot = atomicAdd(s_qn, 1u);
+            if (slot < kQueueCap) {
+              *reinterpret_cast<volatile long long*>(s_q + slot) =
+                  kQueueFlag | kChangeFlag | ((row0 + 128 * mb + p) << 16) | ((long long)(old + 1) << 8) | bi;
+              chg = false;
+            }
           }
           const unsigned int pend = __ballot_sync(0xffffffffu, chg && !no_sums);
           if (pend)

@@ -96,3 +96,45 @@ def test_filter_scores_full_size_no_races():
     cmax = np.sqrt((c.astype(np.float32).astype(np.float64) ** 2).sum(1)).max()
     ratio = np.abs(got - want) / ((nx + cmax) ** 2)[:, None]
     assert float(ratio.max()) <= max((m + 8 + 48) * 2.0 ** -23, 2.0 ** -18) / 4
+
+
+def _coef(m):
+    mp = 7 if m <= 7 else 15 if m <= 15 else 23 if m <= 23 else 31
+    ks = (mp + 1 + 7) // 8
+    return max((m + 8 + 12 * ks) * 2.0 ** -23, 2.0 ** -18)
+
+
+@pytest.mark.parametrize("log_ratio", [-8, -12, -16, -18, -20, -22, -24, -26, -30])
+@pytest.mark.parametrize("signs", ["same", "alternating"])
+def test_filter_bound_adversarial_alignment(log_ratio, signs):
+    """Adversarial inputs for the tensor core's internal adder: in every MMA k-step one large
+    product next to 24 small ones (ratio 2^log_ratio), all of one sign (maximal truncation
+    loss if the adder drops bits below the largest product) or alternating (cancellation).
+    The certified coefficient must cover the worst case for every ratio — i.e. the bound does not
+    rely on the error averaging out, whatever alignment width the hardware adder keeps."""
+    n, m, k = 4096, 25, 16
+    rng = np.random.default_rng(abs(log_ratio) * 7 + (signs == "same"))
+    r = 2.0 ** (log_ratio / 2)  # per-operand ratio: small products = r² × the large one
+    big = rng.uniform(1.0, 2.0, size=n)
+    x = np.empty((n, m))
+    x[:, 0] = big
+    x[:, 1:] = r * rng.uniform(1.0, 2.0, size=(n, m - 1))
+    c = np.empty((k, m))
+    c[:, 0] = -rng.uniform(1.0, 2.0, size=k)
+    c[:, 1:] = -r * rng.uniform(1.0, 2.0, size=(k, m - 1))
+    if signs == "alternating":
+        x[:, 1::2] *= -1.0
+    x = x.astype(np.float32)
+    # the big feature first in a point, but also rotated into other k-step positions
+    for i in range(1, 8):
+        x[i * 512:(i + 1) * 512] = np.roll(x[i * 512:(i + 1) * 512], 3 * i, axis=1)
+    eng = native().NativeEngine(0)
+    eng.load(x)
+    got = eng.debug_filter_scores(c)
+    eng.close()
+    want = exact_scores(x, c)
+    nx = np.sqrt((x.astype(np.float64) ** 2).sum(1))
+    cmax = np.sqrt((c.astype(np.float32).astype(np.float64) ** 2).sum(1)).max()
+    worst = float((np.abs(got - want) / ((nx + cmax) ** 2)[:, None]).max())
+    print(f"ratio 2^{log_ratio} {signs}: worst {worst:.3e} (certified {_coef(m):.3e})")
+    assert worst <= _coef(m) / 4
