@@ -304,6 +304,9 @@ def run_ours(args):
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
+        # NCCL init logging on (stderr): the communicator's nranks / transport are checkable
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local), rank=rank, world_size=world)
     n, m, k, desc = CONFIGS[args.config]
     x, c0, total, lo, hi = load_rows(args, world, rank)

@@ -50,7 +50,7 @@ constexpr long long kQueueFlag = 1ll << 62;
 // (old + 1) << 8 | new.  The recheck warp applies its exact Δ off the epilogue's critical path.
 constexpr long long kChangeFlag = 1ll << 61;
 #ifndef KM_QUEUE_CHANGES
-#define KM_QUEUE_CHANGES 1
+#define KM_QUEUE_CHANGES 0
 #endif
 constexpr int kTileRows = 128;
 #ifndef KM_TRANSFORM_GROUPS
@@ -399,7 +399,9 @@ template <int KP, int MB, int HW = 32, int AS = 0, bool K3 = false>
 struct TcTmem {
   static constexpr int per = MB * (K3 ? 1 : 2) * KP;                       // score columns per tile
   static constexpr int ktail = (HW + 15) / 16;                             // K3: k-steps of the xh·wl tail
-  static constexpr int arow = K3 ? HW + 8 * ktail : HW;                    // A columns per row (TS)
+  // A columns per row (TS): [xh | xl] — the K3 tail MMA re-reads the xh columns (A at a column
+  // offset), so no third copy is stored
+  static constexpr int arow = HW;
   static constexpr int acols = AS * MB * arow;                             // TS: A buffers
   static constexpr int NS0 = (512 - acols) / per;
   static constexpr int NS = NS0 >= 8 ? 8 : NS0;                            // TMEM score buffers
@@ -866,8 +868,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
                 mma_f16_ts(dcol, at + 8 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
               if constexpr (K3) {
 #pragma unroll
-                for (int ks = 0; ks < TM::ktail; ++ks)  // + xh · wl, same accumulator
-                  mma_f16_ts(dcol, at + L::HW + 8 * ks, bdescL + 2 * ks, idesc, 1u);
+                for (int ks = 0; ks < TM::ktail; ++ks)  // + xh · wl (the xh columns again), same accumulator
+                  mma_f16_ts(dcol, at + 8 * ks, bdescL + 2 * ks, idesc, 1u);
               }
             } else {
               const uint64_t adesc0 = make_desc(a0 + sa * (TR * 128) + mb * (128 * 128), 16, 1024);
@@ -951,24 +953,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           for (int q = 0; q < L::HW / 2; ++q) {
             const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
             const float2 hf = __half22float2(h2);
-            const __half2 l2 = __floats2half2_rn(xs[2 * q] - hf.x, xs[2 * q + 1] - hf.y);
+            // x − fl(xh) for both lanes in one packed FADD2
+            const float2 d = __fadd2_rn(make_float2(xs[2 * q], xs[2 * q + 1]), make_float2(-hf.x, -hf.y));
+            const __half2 l2 = __floats2half2_rn(d.x, d.y);
             hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
             lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
           }
           if constexpr (TS) {
             // the point's A row [xh | xl] (HW 32-bit columns) → TMEM lane p of this tile's A buffer
             const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + TM::a_base + (uint32_t)(sa * TM::arow);
-            tmem_st_row<L::HW / 2>(ta, hw);
+            tmem_st_row<L::HW / 2>(ta, hw);             // [xh | xl]
             tmem_st_row<L::HW / 2>(ta + L::HW / 2, lw);
-            if constexpr (K3) {  // [xh | xl | xh | 0-pad to whole k-steps]
-              tmem_st_row<L::HW / 2>(ta + L::HW, hw);
-              if constexpr (TM::arow > L::HW + L::HW / 2) {
-                uint32_t z[TM::arow - L::HW - L::HW / 2];
-#pragma unroll
-                for (int c = 0; c < TM::arow - L::HW - L::HW / 2; ++c) z[c] = 0u;
-                tmem_st_row<TM::arow - L::HW - L::HW / 2>(ta + L::HW + L::HW / 2, z);
-              }
-            }
           } else {
             unsigned char* s_ab = s_a + mb * (128 * 128);
 #pragma unroll
