@@ -49,6 +49,9 @@ constexpr long long kQueueFlag = 1ll << 62;
 // a queue entry of a point whose label CHANGED (not a recheck): flag | change | row << 16 |
 // (old + 1) << 8 | new.  The recheck warp applies its exact Δ off the epilogue's critical path.
 constexpr long long kChangeFlag = 1ll << 61;
+#ifndef KM_HEAVY_PASSES
+#define KM_HEAVY_PASSES 1
+#endif
 #ifndef KM_QUEUE_CHANGES
 #define KM_QUEUE_CHANGES 0
 #endif
@@ -611,6 +614,31 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int 
   }
 }
 
+// Heavy-pass Δ (many labels change): the changed points of one warp read their rows from the
+// pass's raw shared-memory tile, which the epilogue (not the transform) releases in heavy passes —
+// lane f takes feature f of each changed point (a short LDS instead of an L2/DRAM round trip).
+// `prow0`: row in the tile of lane 0's point; rows past the tile's 16-byte bulk come from global.
+static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__ rs, uint32_t bulk_elems,
+                                                       const float* __restrict__ gx_tile, int m, int prow0, int lane,
+                                                       int bi, int old, unsigned int pend, unsigned long long* s_acc,
+                                                       int km, float scale_f, double scale_d, bool use_dscale) {
+  while (pend) {
+    const int j = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const int nb = __shfl_sync(0xffffffffu, bi, j), ob = __shfl_sync(0xffffffffu, old, j);
+    if (lane < m) {
+      const uint32_t e = (uint32_t)(prow0 + j) * m + lane;
+      const float v = e < bulk_elems ? rs[e] : __ldg(gx_tile + e);
+      const long long q = use_dscale ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f));
+      smem_add64(s_acc + (size_t)nb * m + lane, (unsigned long long)q);
+      if (ob >= 0) smem_add64(s_acc + (size_t)ob * m + lane, (unsigned long long)(-q));
+    } else if (lane == m) {
+      smem_add64(s_acc + (size_t)km + nb, 1ull);
+      if (ob >= 0) smem_add64(s_acc + (size_t)km + ob, ~0ull);
+    }
+  }
+}
+
 template <int MT, int KP, bool PRE>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
   static_assert(kThreadsTC == (kTransformWarps + kEpiWarps + 4) * 32, "warp-role layout");
@@ -723,6 +751,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   const double tol = st->tol;
   bool full = a.full != 0;
   const bool no_sums = a.no_sums != 0;
+  // Heavy passes (many label changes): the raw tile stays until the epilogue, which takes the
+  // changed points' rows from shared memory.  Decided per CTA from its previous pass's changes
+  // (the first pass after a separate L0 pass, and full first passes, are heavy).
+  __shared__ int s_heavy;
+  __shared__ unsigned int s_pass_changes;
+  if (tid == 0) {
+    s_heavy = KM_HEAVY_PASSES && !no_sums && (a.full || (resident && a.skip_first)) ? 1 : 0;
+    s_pass_changes = 0u;
+  }
+  __syncthreads();
   int cb = 0;      // resident: s_cbuf half holding C_t
   int g0 = 0;      // tiles of earlier passes (ring positions continue across passes)
   int issued = 0;  // producer: tiles of the current pass already in flight
@@ -736,6 +774,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     // first pass + cluster-sums launch, so iteration 0 starts at the tail with Δ = 0)
     const int pass_tiles = (resident && it == 0 && a.skip_first) ? 0 : my_tiles;
     last_pass_tiles = pass_tiles;
+    const bool heavy = s_heavy != 0;
     const double* C = resident ? s_cbuf + cb * km : a.c64;
     if (pst && it < 256 && blockIdx.x == 0) pst[it * 8 + 0] = globaltimer();
     if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2] = (long long)globaltimer();
@@ -976,9 +1015,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           }
         }
         // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
-        // the TMA producer may refill it
+        // the TMA producer may refill it (heavy passes: the epilogue releases it)
         __syncwarp();
-        if (lane == 0) mbar_arrive(empty_raw + s);
+        if (lane == 0 && !heavy) mbar_arrive(empty_raw + s);
         if (stamp) ts[2] = clock64();
         if constexpr (TS) {
           tmem_st_wait();      // the A row is in TMEM
@@ -1169,12 +1208,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             }
           }
           const unsigned int pend = __ballot_sync(0xffffffffu, chg && !no_sums);
-          if (pend)
-            delta_rows(a.x, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, s_acc, km, scale_f, scale_d,
-                       use_dscale);
+          if (pend) {
+            if (heavy)
+              delta_rows_smem(raw + (g % RS) * (S.raw_stride / 4), (((uint32_t)rows * m * 4u) & ~15u) >> 2,
+                              a.x + row0 * m, m, 128 * mb + (p & ~31), lane, bi, old, pend, s_acc, km, scale_f,
+                              scale_d, use_dscale);
+            else
+              delta_rows(a.x, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, s_acc, km, scale_f, scale_d,
+                         use_dscale);
+          }
+        }
+        if (heavy) {  // the raw tile's rows are no longer needed: the TMA producer may refill it
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty_raw + g % RS);
         }
         if (stamp) ts[6] = clock64();
       }
+      unsigned int my_changed_all = my_changed;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) my_changed_all += __shfl_xor_sync(0xffffffffu, my_changed_all, o);
       unsigned int w2 = full ? 0u : my_changed, w3 = my_rechecked;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
@@ -1182,6 +1234,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         w3 += __shfl_xor_sync(0xffffffffu, w3, o);
       }
       if (lane == 0 && w2) atomicAdd(&st->changed, (unsigned long long)w2);
+      if (lane == 0 && my_changed_all) atomicAdd(&s_pass_changes, my_changed_all);
       if (lane == 0 && w3) atomicAdd(&st->rechecked, (unsigned long long)w3);
       __threadfence_block();
       __syncwarp();
@@ -1190,6 +1243,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     // ===================== tail (all warps) =====================
     tc_fence_before();
     __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
+    if (tid == 0 && pass_tiles > 0) {  // the next pass is heavy if this one changed > 1/256 of the CTA's points
+      s_heavy = KM_HEAVY_PASSES && !no_sums && s_pass_changes * 256u > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
+      s_pass_changes = 0u;
+    }
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
     if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2 + 1] = (long long)globaltimer();
     double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
