@@ -194,6 +194,22 @@ KM_API int km_step_loop_check(km_engine* e);
 KM_API int km_step_loop_state(km_engine* e, int32_t* out4);
 KM_API int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, int64_t* labels_out);
 
+/* Resident form of the row-sharded loop (the fast path): one cooperative launch per GPU runs
+ * the whole Lloyd loop, and every iteration's (k·m + k) int64 Δ is exchanged INSIDE the kernel
+ * over NVLink peer memory — each rank pushes its Δ into every rank's exchange buffer (CUDA IPC
+ * mapping) and sums the `world` rows it receives — instead of an allreduce launch per iteration.
+ *   km_peer_init      allocate this rank's exchange buffer for k; export its IPC handle (64 bytes)
+ *   km_peer_connect   map every rank's buffer (handles[world][64], gathered by the caller)
+ *   km_lloyd_peer     run from C0 until the loop is done or needs the host (empty clusters)
+ *   km_lloyd_peer_resume   after the global repair (km_step_repair_*) and km_step_loop_check
+ * state_out4 = {t, done, converged, need_host}; results through km_step_read.  Every rank must
+ * call these in lockstep with the same C0 / max_iters / tol and a global km_set_frac_bits. */
+KM_API int km_peer_init(km_engine* e, int32_t world, int32_t rank, int32_t k, void* handle_out);
+KM_API int km_peer_connect(km_engine* e, const void* handles);
+KM_API int km_lloyd_peer(km_engine* e, const double* c0, int32_t k, int32_t max_iters, double tol,
+                         int32_t* state_out4);
+KM_API int km_lloyd_peer_resume(km_engine* e, int32_t* state_out4);
+
 KM_API int km_get_stats(km_engine* e, km_stats* out);
 KM_API int km_reset_stats(km_engine* e);
 /* Kernel path for the fused pass: 0 = auto (tcgen05 tensor-core pass when the

@@ -95,6 +95,10 @@ SIGNATURES = {
     "km_step_label_of": (ctypes.c_int, [P, I64, ctypes.POINTER(I32)]),
     "km_step_check": (ctypes.c_int, [P, F64, ctypes.POINTER(I32)]),
     "km_step_read": (ctypes.c_int, [P, P, P, P]),
+    "km_peer_init": (ctypes.c_int, [P, I32, I32, I32, P]),
+    "km_peer_connect": (ctypes.c_int, [P, P]),
+    "km_lloyd_peer": (ctypes.c_int, [P, P, I32, I32, F64, P]),
+    "km_lloyd_peer_resume": (ctypes.c_int, [P, P]),
     "km_get_stats": (ctypes.c_int, [P, ctypes.POINTER(KmStats)]),
     "km_reset_stats": (ctypes.c_int, [P]),
     "km_set_kernel_path": (ctypes.c_int, [P, I32]),
@@ -256,6 +260,29 @@ class NativeEngine:
 
     def loop_check(self):
         self._check(self._lib.km_step_loop_check(self._h))
+
+    # -- row-sharded resident loop, in-kernel NVLink exchange (km_peer_*) ----------------------
+    def peer_init(self, world: int, rank: int, k: int) -> bytes:
+        """Allocate this rank's exchange buffer; returns its 64-byte CUDA IPC handle."""
+        h = ctypes.create_string_buffer(64)
+        self._check(self._lib.km_peer_init(self._h, int(world), int(rank), int(k), h))
+        return h.raw
+
+    def peer_connect(self, handles) -> None:
+        """Map every rank's exchange buffer (handles in rank order, 64 bytes each)."""
+        buf = ctypes.create_string_buffer(b"".join(bytes(h) for h in handles))
+        self._check(self._lib.km_peer_connect(self._h, buf))
+
+    def lloyd_peer(self, c0: np.ndarray, max_iters: int, tol: float):
+        c0 = np.ascontiguousarray(c0, dtype=np.float64)
+        out = np.zeros(4, dtype=np.int32)
+        self._check(self._lib.km_lloyd_peer(self._h, _ptr(c0), c0.shape[0], int(max_iters), float(tol), _ptr(out)))
+        return int(out[0]), bool(out[1]), bool(out[2]), bool(out[3])
+
+    def lloyd_peer_resume(self):
+        out = np.zeros(4, dtype=np.int32)
+        self._check(self._lib.km_lloyd_peer_resume(self._h, _ptr(out)))
+        return int(out[0]), bool(out[1]), bool(out[2]), bool(out[3])
 
     def loop_state(self):
         """(t, done, converged, need_host) — one device→host read."""

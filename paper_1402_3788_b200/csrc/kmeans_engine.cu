@@ -106,6 +106,14 @@ struct km_engine {
   const char* times_path = nullptr; // KM_TC_TIMES
   size_t sums_key = 0;              // cluster-sums launch geometry cache
   bool resident_zeroed = false;     // grid barrier + delta buffers are zero (next resident launch)
+  // row-sharded multi-GPU resident loop (km_peer_*): in-kernel Δ exchange over NVLink peer memory
+  int32_t world = 1, rank = 0;
+  unsigned long long* xch = nullptr;         // this rank's exchange buffer (IPC-exported)
+  size_t xch_nacc = 0;                       // k·m + k it was sized for
+  unsigned long long** xch_peers_dev = nullptr;  // device array [world] of every rank's buffer
+  std::vector<void*> xch_opened;             // IPC mappings of the peers' buffers
+  uint32_t epoch = 0;                        // run id of the exchange's sequence flags
+  bool peer_active = false;                  // the current km_lloyd_peer call uses the exchange
   void* pin = nullptr;              // pinned staging of the resident loop's C0 / model
   size_t pin_cap = 0;
   int sums_per_sm = 1;
@@ -336,6 +344,19 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   a.resident = resident ? 1 : 0;
   a.grid_sync = e->grid_sync;
   a.dlt = e->dlt;
+  if (resident && e->peer_active) {
+    a.xch_peers = e->xch_peers_dev;
+    a.xch_local = e->xch;
+    a.world = e->world;
+    a.rank = e->rank;
+    a.epoch = e->epoch;
+  } else {
+    a.xch_peers = nullptr;
+    a.xch_local = nullptr;
+    a.world = 1;
+    a.rank = 0;
+    a.epoch = 0;
+  }
   if (resident && !e->resident_zeroed) {  // (the begin kernel zeroed them for the first launch of a run)
     CK(cudaMemsetAsync(e->grid_sync, 0, 16, e->stream));
     CK(cudaMemsetAsync(e->dlt, 0, 3 * 8 * ((size_t)e->k * e->m + e->k), e->stream));
@@ -893,11 +914,14 @@ int km_create(int32_t device, km_engine** out) {
   return KM_OK;
 }
 
+static void peer_release(km_engine* e);
+
 int km_destroy(km_engine* e) {
   if (!e) return KM_OK;
   cudaSetDevice(e->device);
   if (e->stream) cudaStreamSynchronize(e->stream);
   drop_points(e);
+  peer_release(e);
   dfree(e->xbuf); dfree(e->stage); dfree(e->labels); dfree(e->recheck_rows); dfree(e->d2);
   dfree(e->labels64); dfree(e->partials);
   dfree(e->pair_best); dfree(e->seed_pv); dfree(e->seed_pi);
@@ -1110,7 +1134,7 @@ int km_converged(km_engine* e, const double* prev, const double* next, int32_t k
 // (state, zeroed accumulators, filter operands), the first pass + cluster sums + the resident
 // launch, and ONE synchronisation that also brings back the state, the centres and the counts
 // (pinned).  Returns KM_RESIDENT_UNFIT when the shape only fits the launch-per-iteration kernel.
-static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double tol) {
+static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double tol, bool resume = false) {
   int r;
   const int k = e->k, m = e->m;
   const size_t km = (size_t)k * m, nacc = km + k;
@@ -1126,21 +1150,23 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
   double* pin_c0 = reinterpret_cast<double*>(e->pin);
   double* pin_c = pin_c0 + km;
   long long* pin_n = reinterpret_cast<long long*>(pin_c + km);
-  std::memcpy(pin_c0, c0, 8 * km);
-  CK(cudaMemcpyAsync(e->cur, pin_c0, 8 * km, cudaMemcpyHostToDevice, e->stream));
-  lloyd_begin_kernel<<<1, 512, 0, e->stream>>>(e->st, max_iters, tol, e->part, e->tot, e->dlt, nacc, e->grid_sync,
-                                               e->recheck_count, e->cur, e->w, e->cn, e->cmax, k, m, e->mpad,
-                                               tc_eligible(e) ? e->wop : nullptr, e->kp, e->pre);
-  CK_LAUNCH("lloyd_begin_kernel launch");
-  e->stats.kernel_launches += 1;
-  e->resident_zeroed = true;
-  e->next_full = true;
+  if (!resume) {
+    std::memcpy(pin_c0, c0, 8 * km);
+    CK(cudaMemcpyAsync(e->cur, pin_c0, 8 * km, cudaMemcpyHostToDevice, e->stream));
+    lloyd_begin_kernel<<<1, 512, 0, e->stream>>>(e->st, max_iters, tol, e->part, e->tot, e->dlt, nacc, e->grid_sync,
+                                                 e->recheck_count, e->cur, e->w, e->cn, e->cmax, k, m, e->mpad,
+                                                 tc_eligible(e) ? e->wop : nullptr, e->kp, e->pre);
+    CK_LAUNCH("lloyd_begin_kernel launch");
+    e->stats.kernel_launches += 1;
+    e->resident_zeroed = true;
+    e->next_full = true;
+  }
   // First pass split in two: L0 = A(C0) writes labels only (tensor cores), then one cluster-sums
   // stream adds every point to its cluster (S(L0) into tot); the resident loop starts at the
   // finish of iteration 1.  (KM_FULL_FIRST_PASS=1: the fused first pass adding every point
   // through the epilogue's shared-memory atomics, kept for A/B timing.)
-  const bool split = !e->full_first_pass;
-  bool full = !split, first = true;
+  const bool split = !e->full_first_pass || e->peer_active;  // (the peer loop exchanges the split's local sums)
+  bool full = !split && !resume, first = !resume;
   DevState* hs = e->st_host;
   for (;;) {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -1181,6 +1207,7 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
     e->next_full = false;
     if (s.done) return KM_OK;
     if (!s.need_host) return set_err(e, KM_ERR_INTERNAL, "resident Lloyd loop stopped without a decision");
+    if (e->peer_active) return KM_OK;  // row shards: the caller runs the global repair (all ranks)
     if ((r = repair_local(e))) return r;
     if ((r = launch_check(e))) return r;
     if ((r = read_state(e))) return r;
@@ -1788,6 +1815,112 @@ int km_step_read(km_engine* e, double* centers_out, int64_t* counts_out, int64_t
   if (counts_out) CK(cudaMemcpyAsync(counts_out, e->model_counts, 8 * (size_t)e->k, cudaMemcpyDeviceToHost, e->stream));
   if (labels_out && (r = download_labels(e, labels_out))) return r;
   CK(cudaStreamSynchronize(e->stream));
+  return KM_OK;
+}
+
+// ---- row-sharded resident loop with the in-kernel NVLink exchange -------------------------
+static void peer_release(km_engine* e) {
+  for (void* p : e->xch_opened) cudaIpcCloseMemHandle(p);
+  e->xch_opened.clear();
+  dfree(e->xch_peers_dev);
+  e->xch_peers_dev = nullptr;
+  dfree(e->xch);
+  e->xch = nullptr;
+  e->xch_nacc = 0;
+  e->world = 1;
+  e->rank = 0;
+}
+
+int km_peer_init(km_engine* e, int32_t world, int32_t rank, int32_t k, void* handle_out) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (world < 1 || rank < 0 || rank >= world) return set_err(e, KM_ERR_CONTRACT, "bad world/rank %d/%d", world, rank);
+  if (k < 1) return set_err(e, KM_ERR_CONTRACT, "k must be >= 1, got %d", k);
+  if (!handle_out) return set_err(e, KM_ERR_CONTRACT, "null handle_out");
+  cudaSetDevice(e->device);
+  peer_release(e);
+  const size_t nacc = (size_t)k * e->m + k;
+  const size_t words = 2 * (size_t)world * nacc + 2 * (size_t)world;
+  int r;
+  if ((r = dalloc(e, &e->xch, 8 * words))) return r;
+  CK(cudaMemset(e->xch, 0, 8 * words));  // sequence flags start below every run's values
+  cudaIpcMemHandle_t h{};
+  CK(cudaIpcGetMemHandle(&h, e->xch));
+  std::memcpy(handle_out, &h, sizeof h);
+  e->world = world;
+  e->rank = rank;
+  e->xch_nacc = nacc;
+  return KM_OK;
+}
+
+int km_peer_connect(km_engine* e, const void* handles) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  if (!e->xch) return set_err(e, KM_ERR_CONTRACT, "call km_peer_init first");
+  if (!handles) return set_err(e, KM_ERR_CONTRACT, "null handles");
+  cudaSetDevice(e->device);
+  std::vector<unsigned long long*> ptrs((size_t)e->world, nullptr);
+  for (int p = 0; p < e->world; ++p) {
+    if (p == e->rank) {
+      ptrs[p] = e->xch;
+      continue;
+    }
+    cudaIpcMemHandle_t h{};
+    std::memcpy(&h, static_cast<const unsigned char*>(handles) + (size_t)p * sizeof h, sizeof h);
+    void* d = nullptr;
+    CK(cudaIpcOpenMemHandle(&d, h, cudaIpcMemLazyEnablePeerAccess));
+    e->xch_opened.push_back(d);
+    ptrs[p] = static_cast<unsigned long long*>(d);
+  }
+  int r;
+  if ((r = dalloc(e, &e->xch_peers_dev, sizeof(void*) * (size_t)e->world))) return r;
+  CK(cudaMemcpy(e->xch_peers_dev, ptrs.data(), sizeof(void*) * (size_t)e->world, cudaMemcpyHostToDevice));
+  return KM_OK;
+}
+
+static void peer_state(km_engine* e, int32_t* out4) {
+  if (!out4) return;
+  out4[0] = e->st_host->t;
+  out4[1] = e->st_host->done;
+  out4[2] = e->st_host->converged;
+  out4[3] = e->st_host->need_host;
+}
+
+int km_lloyd_peer(km_engine* e, const double* c0, int32_t k, int32_t max_iters, double tol, int32_t* state_out4) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  int r;
+  if (!e->x) return set_err(e, KM_ERR_CONTRACT, "no points loaded");
+  if (!e->xch_peers_dev) return set_err(e, KM_ERR_CONTRACT, "call km_peer_init and km_peer_connect first");
+  if (max_iters < 1) return set_err(e, KM_ERR_CONTRACT, "max_iters must be >= 1, got %d", max_iters);
+  if (!(tol >= 0.0)) return set_err(e, KM_ERR_CONTRACT, "tol must be >= 0, got %g", tol);
+  if ((r = check_centers(e, c0, k))) return r;
+  if ((size_t)k * e->m + k != e->xch_nacc) return set_err(e, KM_ERR_CONTRACT, "k differs from km_peer_init's");
+  if ((r = ensure_k(e, k))) return r;
+  scale_for_centers(e, c0, k);
+  if (!use_tc(e) || e->resident_unfit)
+    return set_err(e, KM_ERR_CAPACITY, "the resident peer loop needs the tensor-core pass (fp32, m <= 31, k <= 128)");
+  e->epoch += 1;
+  e->peer_active = true;
+  r = lloyd_resident(e, c0, max_iters, tol);
+  e->peer_active = false;
+  if (r == KM_RESIDENT_UNFIT) {
+    e->resident_unfit = true;
+    return set_err(e, KM_ERR_CAPACITY, "shape does not fit the resident loop");
+  }
+  if (r) return r;
+  peer_state(e, state_out4);
+  return KM_OK;
+}
+
+int km_lloyd_peer_resume(km_engine* e, int32_t* state_out4) {
+  if (!e) return set_err(nullptr, KM_ERR_CONTRACT, "null engine");
+  cudaSetDevice(e->device);
+  if (!e->xch_peers_dev || !e->part) return set_err(e, KM_ERR_CONTRACT, "call km_lloyd_peer first");
+  e->peer_active = true;
+  const int r = lloyd_resident(e, nullptr, 0, 0.0, true);
+  e->peer_active = false;
+  if (r) return r;
+  peer_state(e, state_out4);
   return KM_OK;
 }
 

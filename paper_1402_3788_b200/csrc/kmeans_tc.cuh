@@ -729,7 +729,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     for (int i = tid; i < kQueueCap; i += nthr) s_q[i] = 0;
     if (resident) {
       for (int i = tid; i < km; i += nthr) s_cbuf[i] = a.c64[i];
-      for (int i = tid; i < nacc; i += nthr) s_tot[i] = a.fin.tot[i];  // totals of the current labels
+      // totals of the current labels (peer loop after a separate first pass: the local sums in
+      // fin.tot are this rank's first contribution to the exchange, the totals start at zero)
+      const bool tot0 = a.xch_peers != nullptr && a.skip_first;
+      for (int i = tid; i < nacc; i += nthr) s_tot[i] = tot0 ? 0ull : a.fin.tot[i];
     }
     if (tid == 0) {
       s_qn[0] = s_qn[1] = s_qn[2] = 0u;
@@ -1306,11 +1309,58 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
     }
     __syncthreads();
-    // running totals of the current labels, per CTA: S_t = S_{t−1} + Δ_t (exact int64)
-    for (int i = tid; i < nacc; i += kThreadsTC) {
-      const unsigned long long v = s_tot[i] + __ldcg(dlt + i);
-      s_tot[i] = v;
-      if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
+    if (a.xch_peers != nullptr) {
+      // ---- row-sharded multi-GPU: exchange this iteration's Δ with every rank over NVLink ----
+      // CTA 0 pushes the rank's complete Δ (the local grid barrier has passed) into slot
+      // t_upd & 1, row `rank`, of every rank's buffer, then releases a sequence flag there; every
+      // CTA of every rank waits for all `world` flags and adds the world rows (exact integers, the
+      // same sum on every rank).  Slots alternate: a rank can be at most one exchange ahead (it
+      // needs this rank's next flag to pass the next exchange), so a slot is never overwritten
+      // while it is being read.
+      const int W = a.world;
+      const size_t slot_words = (size_t)W * nacc;
+      const int slot = t_upd & 1;
+      const unsigned long long seq = ((unsigned long long)a.epoch << 32) | (unsigned long long)(unsigned)(t_upd + 1);
+      if (blockIdx.x == 0) {
+        const bool add_local_sums = it == 0 && a.skip_first;
+        for (int pr = 0; pr < W; ++pr) {
+          unsigned long long* dst = a.xch_peers[pr] + slot * slot_words + (size_t)a.rank * nacc;
+          for (int i = tid; i < nacc; i += kThreadsTC)
+            dst[i] = __ldcg(dlt + i) + (add_local_sums ? a.fin.tot[i] : 0ull);
+        }
+        __threadfence_system();
+        __syncthreads();
+        if (tid < W) {
+          unsigned long long* flag = a.xch_peers[tid] + 2 * slot_words + slot * W + a.rank;
+          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
+        }
+      }
+      if (tid < W) {  // bounded wait (a rank that never arrives traps instead of hanging the GPU)
+        const unsigned long long* flag = a.xch_local + 2 * slot_words + slot * W + tid;
+        const long long t0 = clock64();
+        for (;;) {
+          unsigned long long v;
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+          if (v >= seq) break;
+          if (clock64() - t0 > (1ll << 35)) __trap();
+        }
+      }
+      __syncthreads();
+      const unsigned long long* rows = a.xch_local + slot * slot_words;
+      for (int i = tid; i < nacc; i += kThreadsTC) {
+        unsigned long long d = 0;
+        for (int r = 0; r < W; ++r) d += __ldcg(rows + (size_t)r * nacc + i);
+        const unsigned long long v = s_tot[i] + d;
+        s_tot[i] = v;
+        if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
+      }
+    } else {
+      // running totals of the current labels, per CTA: S_t = S_{t−1} + Δ_t (exact int64)
+      for (int i = tid; i < nacc; i += kThreadsTC) {
+        const unsigned long long v = s_tot[i] + __ldcg(dlt + i);
+        s_tot[i] = v;
+        if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
+      }
     }
     __syncthreads();
     const unsigned long long* tot = s_tot;

@@ -45,6 +45,14 @@ struct TcArgs {
   int32_t resident;        // 1: run the whole loop in this (cooperative) launch, see lloyd_pass_tc_kernel
   unsigned int* grid_sync; // resident: [0] barrier arrivals (zeroed before the launch)
   unsigned long long* dlt; // resident: [3][k·m + k] per-pass deltas (zeroed before the launch)
+  // Row-sharded multi-GPU resident loop: after its local grid barrier every rank pushes its Δ
+  // into every rank's exchange buffer over NVLink peer memory (CUDA IPC mappings) and sums the
+  // `world` rows it received — one fused compute + all-reduce per iteration, no collective launch.
+  // Buffer of each rank: [2 slots][world][k·m + k] u64 data, then [2][world] u64 sequence flags.
+  unsigned long long* const* xch_peers;  // device array [world]: each rank's exchange buffer (null: single GPU)
+  unsigned long long* xch_local;         // this rank's exchange buffer
+  int32_t world, rank;
+  uint32_t epoch;                        // run id (identical on every rank, new per km_lloyd_peer call)
   DevState* st;
   int32_t gate;
   float* dbg_scores;       // optional n × k raw tensor-core scores, unscaled (tests)

@@ -57,6 +57,11 @@ class TorchCollective:
         self.dist.all_gather(out, t, group=self.group)
         return np.stack([o.cpu().numpy() for o in out])
 
+    def allgather_bytes(self, blob: bytes) -> list:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, bytes(blob), group=self.group)
+        return out
+
     def exclusive_prefix(self, value: int) -> int:
         sizes = self.allgather_f64(np.array([float(value)]))[:, 0]
         return int(sizes[: self.rank].sum())
@@ -105,11 +110,17 @@ def _global_repair(engine, coll, k, row_offset):
     return len(empties)
 
 
-def run_sharded(engine, coll, c0, max_iters=1000, tol=0.0, want_labels=True) -> ShardResult:
+def run_sharded(engine, coll, c0, max_iters=1000, tol=0.0, want_labels=True, resident=True) -> ShardResult:
     """engine.iterate semantics (engine.py:320-343) over row shards.
 
     `engine` holds this rank's shard (NativeEngine in production); `coll` is
     a TorchCollective.  Returns the replicated model and this rank's labels.
+
+    Fast path (`resident`, CUDA engine, tensor-core shapes): one resident launch per GPU runs the
+    loop and exchanges every iteration's Δ inside the kernel over NVLink peer memory
+    (_run_resident_peer); the collective is only used to set up the IPC mappings, for the
+    one-off agreements (n, max|x|) and for empty-cluster repairs.  Otherwise: per-iteration NCCL
+    allreduce of the partial buffer (batched device-state loop, or the plain step loop).
     """
     c0 = np.ascontiguousarray(c0, dtype=np.float64)
     k = c0.shape[0]
@@ -125,6 +136,8 @@ def run_sharded(engine, coll, c0, max_iters=1000, tol=0.0, want_labels=True) -> 
     row_offset = coll.exclusive_prefix(n_local)
     absmax = float(coll.allreduce_scalar(float(engine.points_info()["absmax"]), "MAX", coll.torch.float64))
     engine.set_frac_bits(engine.frac_bits_for(absmax, n_total))  # one global fixed-point scale
+    if resident and hasattr(engine, "lloyd_peer") and _peer_capable(engine, k):
+        return _run_resident_peer(engine, coll, c0, k, max_iters, tol, want_labels, row_offset)
     engine.step_begin(c0)
     part = partials_tensor(engine)
     if hasattr(engine, "loop_begin"):  # device-state loop: a few iterations per host round trip
@@ -178,6 +191,33 @@ def _run_batched(engine, coll, part, k, max_iters, tol, want_labels, row_offset)
             batch = 1
             continue
         batch = min(batch * 2, 16)
+    centers, counts, labels = engine.step_read(k, want_labels=want_labels)
+    return ShardResult(centers, counts, labels, t, conv, row_offset)
+
+
+def _peer_capable(engine, k) -> bool:
+    """The resident peer loop runs the tensor-core pass: fp32 points, m <= 31, k <= 128."""
+    info = engine.points_info()
+    return info["point_bytes"] == 4 and info["m"] <= 31 and k <= 128
+
+
+def _run_resident_peer(engine, coll, c0, k, max_iters, tol, want_labels, row_offset) -> ShardResult:
+    """Every rank's resident kernel runs the Lloyd loop on its shard; per iteration its Δ goes to
+    every rank's exchange buffer over NVLink (CUDA IPC, km_peer_*) and each rank sums the `world`
+    rows itself — exact integers, so the model is bit-identical on every rank and to one GPU.  The
+    kernels stop together (identical totals ⇒ identical decisions) when the loop is done or has
+    empty clusters; those take the global repair here, then the loop resumes."""
+    handle = engine.peer_init(coll.world, coll.rank, k)
+    engine.peer_connect(coll.allgather_bytes(handle))
+    t, done, conv, need_host = engine.lloyd_peer(c0, max_iters, tol)
+    while not done:
+        if need_host:
+            _global_repair(engine, coll, k, row_offset)
+            engine.loop_check()
+            t, done, conv, _ = engine.loop_state()
+            if done:
+                break
+        t, done, conv, need_host = engine.lloyd_peer_resume()
     centers, counts, labels = engine.step_read(k, want_labels=want_labels)
     return ShardResult(centers, counts, labels, t, conv, row_offset)
 
