@@ -30,10 +30,7 @@ namespace km {
 constexpr int kSumsWarps = 16;                      // consumer warps (+ one producer warp)
 constexpr int kSumsThreads = (kSumsWarps + 1) * 32;
 constexpr int kSumsTile = 128;                      // rows per bulk tile (kSumsWarps × 8)
-#ifndef KM_SUMS_STAGES
-#define KM_SUMS_STAGES 4
-#endif
-constexpr int kSumsStages = KM_SUMS_STAGES;         // tiles in flight per CTA
+constexpr int kSumsStages = 4;                      // tiles in flight per CTA
 
 // shared memory: [stages] × (row tile + labels) ring, then the accumulators
 __host__ __device__ inline size_t sums_stage_bytes(int m) {
@@ -78,36 +75,9 @@ __device__ __forceinline__ void sums_rows_full(const float* __restrict__ sxw, co
   }
 }
 
-// k ≤ 16: every lane keeps its feature's 16 cluster sums in REGISTERS, the (warp-uniform) label
-// selects one through a jump table — no shared-memory accumulator traffic per row (the 64-bit
-// LDS + STS of the accumulator were 4 of the ~6 shared-memory wavefronts per row, the kernel's
-// bound).  Case bodies index the array with constants, so it stays in registers.
-#define KM_SUMS_CASE(c) \
-  case c:               \
-    acc[c] += q;        \
-    break;
-template <int MT, int RPW>
-__device__ __forceinline__ void sums_rows_reg(const float* __restrict__ sxw, const int32_t* __restrict__ slw,
-                                              int lane, unsigned long long (&acc)[16], float scale_f, float cnt_v) {
-  const bool feat = lane < MT;
-#pragma unroll
-  for (int j = 0; j < RPW; ++j) {
-    const int L = slw[j];
-    const float v = feat ? sxw[j * MT] : cnt_v;
-    const unsigned long long q = (unsigned long long)__float2ll_rn(__fmul_rn(v, scale_f));
-    switch (L) {
-      KM_SUMS_CASE(0) KM_SUMS_CASE(1) KM_SUMS_CASE(2) KM_SUMS_CASE(3) KM_SUMS_CASE(4) KM_SUMS_CASE(5)
-      KM_SUMS_CASE(6) KM_SUMS_CASE(7) KM_SUMS_CASE(8) KM_SUMS_CASE(9) KM_SUMS_CASE(10) KM_SUMS_CASE(11)
-      KM_SUMS_CASE(12) KM_SUMS_CASE(13) KM_SUMS_CASE(14) KM_SUMS_CASE(15)
-      default: break;
-    }
-  }
-}
-#undef KM_SUMS_CASE
-
 // MT > 0: compile-time feature count (the full-tile fast path); MT = 0: runtime m
 template <int MT, bool PRIV, bool USE_D>
-__global__ void __launch_bounds__(kSumsThreads, 2) cluster_sums_f32_kernel(
+__global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
     const float* __restrict__ x, const int32_t* __restrict__ labels, int64_t n, int m, int k, float scale_f,
     double scale_d, unsigned long long* __restrict__ out /* [k·m sums][k counts] */) {
   extern __shared__ __align__(1024) unsigned char s_raw[];
@@ -148,10 +118,6 @@ __global__ void __launch_bounds__(kSumsThreads, 2) cluster_sums_f32_kernel(
     if (lb) tc::bulk_g2s_hint(dst + xbytes_max, labels + row0, lb, full + s, pol);
   };
   constexpr int RPW = kSumsTile / kSumsWarps;  // rows per warp and tile
-  const bool reg_acc = MT > 0 && !USE_D && k <= 16;  // register accumulators (full tiles)
-  unsigned long long racc[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) racc[c] = 0ull;
   const float cnt_v = 1.0f / scale_f;          // = 2^-F: converts to exactly 1 (the count lane)
   if (warp == kSumsWarps) {  // producer warp: one thread keeps the ring full
     if (lane == 0)
@@ -173,11 +139,7 @@ __global__ void __launch_bounds__(kSumsThreads, 2) cluster_sums_f32_kernel(
         for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsWarps * 32) sl[e] = __ldg(labels + row0 + e);
         tc::named_bar_sync(1, kSumsWarps * 32);
       }
-      if (reg_acc && rows == kSumsTile) {
-        if (active)
-          sums_rows_reg<(MT > 0 ? MT : 1), RPW>(sx + warp * RPW * MT + (lane < m ? lane : 0), sl + warp * RPW, lane,
-                                               racc, scale_f, cnt_v);
-      } else if (MT > 0 && !USE_D && rows == kSumsTile) {
+      if (MT > 0 && !USE_D && rows == kSumsTile) {
         if (active)
           sums_rows_full<(MT > 0 ? MT : 1), RPW, PRIV>(sx + warp * RPW * MT + (lane < m ? lane : 0), sl + warp * RPW, lane,
                                                        acc + lane, scale_f, cnt_v);
@@ -187,15 +149,6 @@ __global__ void __launch_bounds__(kSumsThreads, 2) cluster_sums_f32_kernel(
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(empty + s);
-    }
-    if (reg_acc && active) {  // the registers into the warp's accumulator (plain adds, once)
-#pragma unroll
-      for (int c = 0; c < 16; ++c) {
-        if (c < k) {
-          unsigned long long* dst = acc + (size_t)c * row_len + lane;
-          if (PRIV) *dst += racc[c]; else smem_add64(dst, racc[c]);
-        }
-      }
     }
   }
   __syncthreads();

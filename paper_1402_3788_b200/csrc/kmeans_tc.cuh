@@ -198,8 +198,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait of a role that is normally ahead of its producer (the epilogue on the MMA): a failed
 // try_wait returns on any barrier event of the CTA, so with 12 epilogue warps waiting the retry
 // loop would take a quarter of the SM's issue slots away from the transform; back off instead.
-// Group waits (tuning knob, off: measured slower — 44.6 vs 43.6 µs per steady pass, the bar.sync
-// hand-off adds latency): in each 4-warp transform / epilogue group only one warp polls the mbarrier (a
+// Group waits (tuning knob: bit 0 epilogue groups, bit 1 transform groups; both on measured slower —
+// 44.6 vs 43.6 µs per steady pass, the bar.sync hand-off adds latency): in each 4-warp group only one warp polls the mbarrier (a
 // failed try_wait wakes on every barrier event of the CTA — with 20 waiting warps the retry loops
 // were ~25% of all issued instructions); the others park in a named barrier (bar.sync issues
 // nothing while blocked) and proceed after tcgen05.fence::after_thread_sync.
@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[0] = clock64();
-        if (KM_GROUP_WAIT) {  // one warp of the group polls both barriers, the other three park in bar.sync
+        if (KM_GROUP_WAIT & 2) {  // one warp of the group polls both barriers, the other three park in bar.sync
           if ((warp & 3) == 0) {
             mbar_wait(full_raw + s, (g / RS) & 1);
             if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
@@ -960,7 +960,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           continue;
         }
         const float* rs = raw + s * (S.raw_stride / 4);
-        if (!KM_GROUP_WAIT && g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+        if (!(KM_GROUP_WAIT & 2) && g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
         if (stamp) ts[7] = clock64();
         unsigned char* s_a = sm + S.off_a + sa * (TR * 128);
 #pragma unroll
@@ -1077,7 +1077,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[4] = clock64();
-        if (KM_GROUP_WAIT) {  // one warp of the group polls the barrier, the other three park in bar.sync
+        if (KM_GROUP_WAIT & 1) {  // one warp of the group polls the barrier, the other three park in bar.sync
           if ((ew & 3) == 0) mbar_wait_backoff(s_full + ss, (g / TM::NS) & 1);
           named_bar_sync(1 + e, 128);
         } else {
@@ -1134,8 +1134,19 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           uint32_t mk[MW];
 #pragma unroll
           for (int w = 0; w < MW; ++w) mk[w] = 0u;
+          if constexpr (KEEP) {
+            // set.le gives an all-ones mask per candidate: one LOP3 + half an IADD3 per centre
+            // accumulate the count and the index sum; the candidate mask is only built for
+            // uncertified points (below)
 #pragma unroll
-          for (int ch = 0; ch < NCH; ++ch) {
+            for (int c = 0; c < KP; ++c) {
+              uint32_t le;
+              asm("set.le.u32.f32 %0, %1, %2;" : "=r"(le) : "f"(vk[c]), "f"(thr));
+              cnt += le & (1u + ((uint32_t)c << 8));
+            }
+          }
+#pragma unroll
+          for (int ch = 0; ch < (KEEP ? 0 : NCH); ++ch) {
             if (!KEEP) {
               uint32_t r0[16], r1[16];
               tmem_ld16(tcol + ch * 16, r0);
@@ -1154,17 +1165,21 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             }
             mk[(ch * 16) >> 5] |= bits << ((ch * 16) & 31);
           }
-          // padded centres (c ≥ k) are never candidates, whatever the threshold (exact_only
-          // sets it to +inf): the recheck only ever reads real centre rows
-#pragma unroll
-          for (int w = 0; w < MW; ++w) {
-            const int lim = k - 32 * w;
-            mk[w] &= lim >= 32 ? 0xffffffffu : lim <= 0 ? 0u : ((1u << lim) - 1u);
-          }
           int bi = (int)(cnt >> 8);
           const bool unc = active && (cnt & 0xff) != 1u && !(KM_DBG_FLAGS & 256);  // (dbg 256: timing only)
           if (__any_sync(0xffffffffu, unc)) {
             if (unc) {
+              if constexpr (KEEP) {  // the candidate mask (uncertified points only)
+#pragma unroll
+                for (int c = 0; c < KP; ++c) mk[c >> 5] |= (vk[c] <= thr ? 1u : 0u) << (c & 31);
+              }
+              // padded centres (c ≥ k) are never candidates, whatever the threshold (exact_only
+              // sets it to +inf): the recheck only ever reads real centre rows
+#pragma unroll
+              for (int w = 0; w < MW; ++w) {
+                const int lim = k - 32 * w;
+                mk[w] &= lim >= 32 ? 0xffffffffu : lim <= 0 ? 0u : ((1u << lim) - 1u);
+              }
               // uncertified: only the candidates can be the reference's argmin (every other
               // centre is strictly farther) — queue the point with its candidate mask
               ++my_rechecked;
