@@ -414,6 +414,23 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
           fprintf(f, "\n");
         }
       }
+      if (resident && h[6144] && h[6444] && h[6744]) {  // is the per-CTA pass time systematic? (passes 100/101/150)
+        double a[3][148];
+        int nb = 0;
+        for (int b = 0; b < 148 && h[6144 + 2 * b]; ++b, ++nb)
+          for (int q = 0; q < 3; ++q) a[q][b] = (double)(h[6144 + 300 * q + 2 * b + 1] - h[6144 + 300 * q + 2 * b]);
+        auto corr = [&](int p, int q) {
+          double mp = 0, mq = 0, spq = 0, spp = 0, sqq = 0;
+          for (int b = 0; b < nb; ++b) { mp += a[p][b]; mq += a[q][b]; }
+          mp /= nb; mq /= nb;
+          for (int b = 0; b < nb; ++b) {
+            spq += (a[p][b] - mp) * (a[q][b] - mq); spp += (a[p][b] - mp) * (a[p][b] - mp); sqq += (a[q][b] - mq) * (a[q][b] - mq);
+          }
+          return spq / std::sqrt(spp * sqq + 1e-30);
+        };
+        fprintf(f, "per-CTA main-loop time correlation: pass100~101 %.3f  pass100~150 %.3f  pass101~150 %.3f\n",
+                corr(0, 1), corr(0, 2), corr(1, 2));
+      }
       if (resident) {  // per-pass phase ends of the resident loop (ns, max over CTAs, from CTA 0's start)
         const unsigned long long* q = reinterpret_cast<const unsigned long long*>(h + 4096);
         double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};

@@ -780,7 +780,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     const bool heavy = s_heavy != 0;
     const double* C = resident ? s_cbuf + cb * km : a.c64;
     if (pst && it < 256 && blockIdx.x == 0) pst[it * 8 + 0] = globaltimer();
-    if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2] = (long long)globaltimer();
+    if (pst && (it == 100 || it == 101 || it == 150))
+      a.dbg_times[6144 + (it == 100 ? 0 : it == 101 ? 300 : 600) + blockIdx.x * 2] = (long long)globaltimer();
     // exact re-decision of queue entry q (thread per point, candidate centres only); Δ into s_acc
     // Δ of a changed point (queued by the epilogue): its row from global memory (L2: streamed
     // moments ago), + to the new cluster, − from the old one
@@ -1135,15 +1136,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
 #pragma unroll
           for (int w = 0; w < MW; ++w) mk[w] = 0u;
           if constexpr (KEEP) {
-            // set.le gives an all-ones mask per candidate: one LOP3 + half an IADD3 per centre
-            // accumulate the count and the index sum; the candidate mask is only built for
-            // uncertified points (below)
+            // count and index sum only (FSETP + predicated add per centre); the candidate mask is
+            // built for uncertified points alone (below)
 #pragma unroll
-            for (int c = 0; c < KP; ++c) {
-              uint32_t le;
-              asm("set.le.u32.f32 %0, %1, %2;" : "=r"(le) : "f"(vk[c]), "f"(thr));
-              cnt += le & (1u + ((uint32_t)c << 8));
-            }
+            for (int c = 0; c < KP; ++c) cnt += vk[c] <= thr ? (1u + ((uint32_t)c << 8)) : 0u;
           }
 #pragma unroll
           for (int ch = 0; ch < (KEEP ? 0 : NCH); ++ch) {
@@ -1266,7 +1262,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       s_pass_changes = 0u;
     }
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
-    if (pst && it == 100) a.dbg_times[6144 + blockIdx.x * 2 + 1] = (long long)globaltimer();
+    if (pst && (it == 100 || it == 101 || it == 150))
+      a.dbg_times[6144 + (it == 100 ? 0 : it == 101 ? 300 : 600) + blockIdx.x * 2 + 1] = (long long)globaltimer();
     double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
     const int stage_cap = (int)(RS * S.raw_stride / 8);
     {
@@ -1315,11 +1312,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       unsigned long long* nxt = a.dlt + (size_t)((it + 1) % 3) * nacc;
       for (int i = tid; i < nacc; i += kThreadsTC) nxt[i] = 0ull;
     }
-    __threadfence();
+    // grid barrier (the cooperative-groups pattern): the CTA's writes are ordered before thread
+    // 0's gpu-scope fence by the CTA barrier, so one fence per CTA (not one per thread) releases them
     __syncthreads();
     if (pst && it < 256) atomicMax(pst + it * 8 + 3, globaltimer());
     if (pst && it < 256) atomicMax(pst + it * 8 + 4, globaltimer());
     if (tid == 0) {
+      __threadfence();
       atomicAdd(a.grid_sync, 1u);
       grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
     }
