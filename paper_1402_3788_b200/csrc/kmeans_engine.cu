@@ -844,22 +844,36 @@ static int download_labels(km_engine* e, int64_t* out) {
 static int launch_sums(km_engine* e, unsigned long long* out) {
   if (e->point_bytes != 4 || e->m > 31) return set_err(e, KM_ERR_INTERNAL, "cluster-sums kernel: fp32, m <= 31 only");
   const size_t per = (size_t)e->k * (e->m + 1) * 8;
-  const bool priv = per * kSumsWarps <= 100 * 1024;  // warp-private accumulators (2 CTAs / SM) where they fit
-  const size_t smem = sums_smem_bytes(e->m, e->k, priv);
-  if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
   const bool use_d = e->frac_bits > 120 || e->frac_bits < -120;
-  // compile-time feature counts for the BASELINE shapes (full tiles at immediate offsets)
-  auto pick = [&](auto mt) {
+  // k ≤ 128: cluster-owner warps with register accumulators (no accumulator smem); larger k: the
+  // shared-memory accumulator kernel (warp-private where they fit)
+  const int kc = e->k <= 16 ? 1 : e->k <= 32 ? 2 : e->k <= 64 ? 4 : e->k <= 128 ? 8 : 0;
+  const bool priv = kc == 0 && per * kSumsWarps <= 100 * 1024;
+  const size_t smem = kc ? sums_smem_bytes(e->m, 0, false) : sums_smem_bytes(e->m, e->k, priv);
+  if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
+  using Kern = void (*)(const float*, const int32_t*, int64_t, int, int, float, double, unsigned long long*);
+  // compile-time feature counts for the BASELINE shapes
+  auto owner = [&](auto mt) -> Kern {
+    constexpr int MT = decltype(mt)::value;
+    switch (kc) {
+      case 1: return use_d ? cluster_sums_owner_kernel<MT, 1, true> : cluster_sums_owner_kernel<MT, 1, false>;
+      case 2: return use_d ? cluster_sums_owner_kernel<MT, 2, true> : cluster_sums_owner_kernel<MT, 2, false>;
+      case 4: return use_d ? cluster_sums_owner_kernel<MT, 4, true> : cluster_sums_owner_kernel<MT, 4, false>;
+      default: return use_d ? cluster_sums_owner_kernel<MT, 8, true> : cluster_sums_owner_kernel<MT, 8, false>;
+    }
+  };
+  auto accum = [&](auto mt) -> Kern {
     constexpr int MT = decltype(mt)::value;
     return priv ? (use_d ? cluster_sums_f32_kernel<MT, true, true> : cluster_sums_f32_kernel<MT, true, false>)
                 : (use_d ? cluster_sums_f32_kernel<MT, false, true> : cluster_sums_f32_kernel<MT, false, false>);
   };
-  auto kern = e->m == 25 ? pick(std::integral_constant<int, 25>{})
+  auto pick = [&](auto mt) -> Kern { return kc ? owner(mt) : accum(mt); };
+  Kern kern = e->m == 25 ? pick(std::integral_constant<int, 25>{})
               : e->m == 10 ? pick(std::integral_constant<int, 10>{})
               : e->m == 5 ? pick(std::integral_constant<int, 5>{})
                           : pick(std::integral_constant<int, 0>{});
   // launch geometry per (k, m) shape, computed once (no attribute / occupancy queries per call)
-  const size_t key = (smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0)) * 64 + (size_t)e->m;
+  const size_t key = ((smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0)) * 64 + (size_t)e->m) * 16 + (size_t)kc;
   if (e->sums_key != key) {
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;

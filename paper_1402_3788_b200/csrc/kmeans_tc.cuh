@@ -145,6 +145,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 #define KM_TC_TUNING 0
 #endif
 #define KM_DBG_FLAGS (KM_TC_TUNING ? a.dbg_flags : 0)
+#ifndef KM_WAIT_TIMEBOUND
+#define KM_WAIT_TIMEBOUND 1
+#endif
+#ifndef KM_TRY_HINT
+#define KM_TRY_HINT 0x100000
+#endif
 #ifndef KM_WAIT_MODE
 #define KM_WAIT_MODE 2
 #endif
@@ -173,7 +179,7 @@ __device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
       "selp.u32 %0, 1, 0, p;\n"
       "}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(0x100000)  // ≤ ~1 ms per attempt
+      : "r"(smem_u32(bar)), "r"(parity), "r"(KM_TRY_HINT)
       : "memory");
   return ok != 0;
 }
@@ -189,6 +195,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (++n == (1u << 26)) __trap();
   }
 #else
+#if KM_WAIT_TIMEBOUND
   // bounded in TIME (a failed try_wait may sleep up to its suspend hint): a deadlocked pipeline
   // traps after ~4 s instead of hanging the device
   if (mbar_try(bar, parity)) return;
@@ -196,6 +203,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) {
     if (clock64() - t0 > (1ll << 33)) __trap();
   }
+#else
+  uint32_t n = 0;
+  while (!mbar_try(bar, parity)) {
+    if (++n == (1u << 22)) __trap();
+  }
+#endif
 #endif
 }
 // Wait of a role that is normally ahead of its producer (the epilogue on the MMA): a failed
