@@ -94,7 +94,6 @@ struct km_engine {
   unsigned int* recheck_count = nullptr;
   unsigned int* cta_done = nullptr;      // fused-finish completion counter
   unsigned int* grid_sync = nullptr;     // resident loop: barrier arrivals
-  unsigned int* pool = nullptr;          // resident loop: [3] dynamic-tail tickets (rotating)
   unsigned long long* dlt = nullptr;     // resident loop: [3][k·m + k] per-pass deltas
   bool resident_unfit = false;           // the resident TC loop does not fit this shape (use per-iteration launches)
   bool last_pass_full = true;       // the most recent pass produced full sums (finish: tot = part)
@@ -103,7 +102,7 @@ struct km_engine {
   // environment knobs, read once at km_create (tuning / A-B experiments only)
   bool full_first_pass = false;     // KM_FULL_FIRST_PASS=1: fused full first pass (epilogue atomics)
   bool no_resident = false;         // KM_NO_RESIDENT=1: launch-per-iteration loop
-  bool no_dyn_tail = false;         // KM_NO_DYN_TAIL=1: static tile ranges only
+  bool sums_owner = false;          // KM_SUMS_OWNER=1: cluster-owner sums kernel (A/B)
   int dbg_flags = 0;                // KM_TC_DBG
   const char* times_path = nullptr; // KM_TC_TIMES
   size_t sums_key = 0;              // cluster-sums launch geometry cache
@@ -346,11 +345,7 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   a.resident = resident ? 1 : 0;
   a.grid_sync = e->grid_sync;
   a.dlt = e->dlt;
-  a.pool = e->pool;
-  {  // dynamic tail of the resident loop: 1/16 of the tiles, when every CTA has ≥ 8 tiles of its own
-    const int64_t ntiles = (e->n + tc::kTile - 1) / tc::kTile;
-    a.pool_tiles = (resident && !e->no_dyn_tail && ntiles >= 8LL * e->num_sms) ? ntiles / 16 : 0;
-  }
+
   if (resident && e->peer_active) {
     a.xch_peers = e->xch_peers_dev;
     a.xch_local = e->xch;
@@ -366,7 +361,6 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   }
   if (resident && !e->resident_zeroed) {  // (the begin kernel zeroed them for the first launch of a run)
     CK(cudaMemsetAsync(e->grid_sync, 0, 16, e->stream));
-    CK(cudaMemsetAsync(e->pool, 0, 16, e->stream));
     CK(cudaMemsetAsync(e->dlt, 0, 3 * 8 * ((size_t)e->k * e->m + e->k), e->stream));
   }
   if (resident) e->resident_zeroed = false;
@@ -625,8 +619,7 @@ static void free_k(km_engine* e) {
   dfree(e->part); dfree(e->cur); dfree(e->prev); dfree(e->model_counts);
   dfree(e->w); dfree(e->cn); dfree(e->cmax); dfree(e->winner);
   dfree(e->scratch_d); dfree(e->wop); dfree(e->tot);
-  dfree(e->recheck_count); dfree(e->cta_done); dfree(e->grid_sync); dfree(e->dlt); dfree(e->pool);
-  e->pool = nullptr;
+  dfree(e->recheck_count); dfree(e->cta_done); dfree(e->grid_sync); dfree(e->dlt);
   e->dlt = nullptr;
   e->part = nullptr; e->cur = nullptr; e->prev = nullptr; e->model_counts = nullptr;
   e->w = nullptr; e->cn = nullptr; e->cmax = nullptr; e->winner = nullptr;
@@ -666,8 +659,6 @@ static int ensure_k(km_engine* e, int32_t k) {
   CK(cudaMemsetAsync(e->recheck_count, 0, 16, e->stream));
   if ((r = dalloc(e, &e->cta_done, 16))) return r;
   if ((r = dalloc(e, &e->grid_sync, 16))) return r;
-  if ((r = dalloc(e, &e->pool, 16))) return r;
-  CK(cudaMemsetAsync(e->pool, 0, 16, e->stream));
   if ((r = dalloc(e, &e->dlt, 3 * 8 * ((size_t)k * m + k)))) return r;
   CK(cudaMemsetAsync(e->cta_done, 0, 16, e->stream));
   CK(cudaMemsetAsync(e->tot, 0, 8 * ((size_t)k * m + k), e->stream));
@@ -847,7 +838,9 @@ static int launch_sums(km_engine* e, unsigned long long* out) {
   const bool use_d = e->frac_bits > 120 || e->frac_bits < -120;
   // k ≤ 128: cluster-owner warps with register accumulators (no accumulator smem); larger k: the
   // shared-memory accumulator kernel (warp-private where they fit)
-  const int kc = e->k <= 16 ? 1 : e->k <= 32 ? 2 : e->k <= 64 ? 4 : e->k <= 128 ? 8 : 0;
+  // (the cluster-owner kernel measured 120 µs vs 70 µs for the accumulator kernel at cfg3 — latency-
+  // bound ballot loops — so it is only selected with KM_SUMS_OWNER=1)
+  const int kc = !e->sums_owner ? 0 : e->k <= 16 ? 1 : e->k <= 32 ? 2 : e->k <= 64 ? 4 : e->k <= 128 ? 8 : 0;
   const bool priv = kc == 0 && per * kSumsWarps <= 100 * 1024;
   const size_t smem = kc ? sums_smem_bytes(e->m, 0, false) : sums_smem_bytes(e->m, e->k, priv);
   if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
@@ -935,7 +928,7 @@ int km_create(int32_t device, km_engine** out) {
   e->device = device;
   e->full_first_pass = getenv("KM_FULL_FIRST_PASS") && atoi(getenv("KM_FULL_FIRST_PASS")) != 0;
   e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
-  e->no_dyn_tail = getenv("KM_NO_DYN_TAIL") != nullptr;
+  e->sums_owner = getenv("KM_SUMS_OWNER") != nullptr;
   e->dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
   e->times_path = getenv("KM_TC_TIMES");
   e->num_sms = prop.multiProcessorCount;
@@ -1197,7 +1190,6 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
     std::memcpy(pin_c0, c0, 8 * km);
     CK(cudaMemcpyAsync(e->cur, pin_c0, 8 * km, cudaMemcpyHostToDevice, e->stream));
     lloyd_begin_kernel<<<1, 512, 0, e->stream>>>(e->st, max_iters, tol, e->part, e->tot, e->dlt, nacc, e->grid_sync,
-                                                 e->pool,
                                                  e->recheck_count, e->cur, e->w, e->cn, e->cmax, k, m, e->mpad,
                                                  tc_eligible(e) ? e->wop : nullptr, e->kp, e->pre);
     CK_LAUNCH("lloyd_begin_kernel launch");

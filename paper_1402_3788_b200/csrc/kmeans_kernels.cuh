@@ -673,8 +673,7 @@ __global__ void __launch_bounds__(512) prep_filter_kernel(const double* c, float
 __global__ void __launch_bounds__(512) lloyd_begin_kernel(DevState* st, int max_iters, double tol,
                                                           unsigned long long* part, unsigned long long* tot,
                                                           unsigned long long* dlt, size_t nacc,
-                                                          unsigned int* grid_sync, unsigned int* pool,
-                                                          unsigned int* recheck_count,
+                                                          unsigned int* grid_sync, unsigned int* recheck_count,
                                                           const double* c, float* w, float* cn, float* cmax, int k,
                                                           int m, int mpad, unsigned short* wop, int kp, float pre) {
   __shared__ float s_red[32];
@@ -684,7 +683,6 @@ __global__ void __launch_bounds__(512) lloyd_begin_kernel(DevState* st, int max_
     s.tol = tol;
     *st = s;
     grid_sync[0] = grid_sync[1] = grid_sync[2] = grid_sync[3] = 0u;
-    pool[0] = pool[1] = pool[2] = pool[3] = 0u;
     *recheck_count = 0u;
   }
   for (size_t i = threadIdx.x; i < nacc; i += blockDim.x) {

@@ -222,14 +222,18 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_owner_kernel(
     const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
     if (warp == 0) tc::mbar_wait(full + s, (i / kSumsStages) & 1);
     tc::named_bar_sync(1, kSumsWarps * 32);
-    const float* sx = reinterpret_cast<const float*>(ring + s * stage);
-    const int32_t* sl = reinterpret_cast<const int32_t*>(ring + s * stage + xbytes_max);
-    const uint32_t xe = (((uint32_t)rows * mm * 4u) & ~15u) >> 2, le = (((uint32_t)rows * 4u) & ~15u) >> 2;
+    float* sx = reinterpret_cast<float*>(ring + s * stage);
+    int32_t* sl = reinterpret_cast<int32_t*>(ring + s * stage + xbytes_max);
+    if (rows < kSumsTile) {  // ragged last tile: patch the sub-granule tail from global memory
+      const uint32_t xe = (((uint32_t)rows * mm * 4u) & ~15u) >> 2, le = (((uint32_t)rows * 4u) & ~15u) >> 2;
+      for (uint32_t e = xe + threadIdx.x; e < (uint32_t)rows * mm; e += kSumsWarps * 32) sx[e] = __ldg(x + row0 * mm + e);
+      for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsWarps * 32) sl[e] = __ldg(labels + row0 + e);
+      tc::named_bar_sync(1, kSumsWarps * 32);
+    }
 #pragma unroll
     for (int q = 0; q < kSumsTile / 32; ++q) {
       const int r = q * 32 + lane;
-      // the ragged last tile: rows past the 16-byte bulk come from global memory
-      const int lab = r < rows ? ((uint32_t)r < le ? sl[r] : __ldg(labels + row0 + r)) : -1;
+      const int lab = r < rows ? sl[r] : -1;
 #pragma unroll
       for (int j = 0; j < KC; ++j) {
         const int c = warp + kSumsWarps * j;
@@ -239,8 +243,7 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_owner_kernel(
           const int b = __ffs(mask) - 1;
           mask &= mask - 1;
           if (feat) {
-            const uint32_t e = (uint32_t)(q * 32 + b) * mm + lane;
-            const float v = e < xe ? sx[e] : __ldg(x + row0 * mm + e);
+            const float v = sx[(q * 32 + b) * mm + lane];
             acc[j] += (unsigned long long)(USE_D ? __double2ll_rn(__dmul_rn((double)v, scale_d))
                                                  : __float2ll_rn(__fmul_rn(v, scale_f)));
           }

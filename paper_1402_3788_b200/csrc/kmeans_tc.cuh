@@ -145,11 +145,8 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 #define KM_TC_TUNING 0
 #endif
 #define KM_DBG_FLAGS (KM_TC_TUNING ? a.dbg_flags : 0)
-#ifndef KM_WAIT_TIMEBOUND
-#define KM_WAIT_TIMEBOUND 1
-#endif
 #ifndef KM_TRY_HINT
-#define KM_TRY_HINT 0x100000
+#define KM_TRY_HINT 0x100000  // try_wait suspend-time hint (ns)
 #endif
 #ifndef KM_WAIT_MODE
 #define KM_WAIT_MODE 2
@@ -195,7 +192,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     if (++n == (1u << 26)) __trap();
   }
 #else
-#if KM_WAIT_TIMEBOUND
   // bounded in TIME (a failed try_wait may sleep up to its suspend hint): a deadlocked pipeline
   // traps after ~4 s instead of hanging the device
   if (mbar_try(bar, parity)) return;
@@ -203,12 +199,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try(bar, parity)) {
     if (clock64() - t0 > (1ll << 33)) __trap();
   }
-#else
-  uint32_t n = 0;
-  while (!mbar_try(bar, parity)) {
-    if (++n == (1u << 22)) __trap();
-  }
-#endif
 #endif
 }
 // Wait of a role that is normally ahead of its producer (the epilogue on the MMA): a failed
@@ -411,6 +401,12 @@ struct TcLayout {
   static constexpr int KSTEPS = (2 * HW) / 16;       // kind::f16 MMA k-steps (16 halfs = 32 B each)
 };
 
+#ifndef KM_K3_SMEM
+#define KM_K3_SMEM 1
+#endif
+#ifndef KM_NS_MAX
+#define KM_NS_MAX 8
+#endif
 // K3: the MMA accumulates all three products (xh·wh + xl·wh + xh·wl) into ONE column per centre
 // (A row [xh | xl | xh], B rows [wh | wh] and [wl]), otherwise hi and lo parts land in two
 // columns that the epilogue adds.
@@ -423,7 +419,7 @@ struct TcTmem {
   static constexpr int arow = HW;
   static constexpr int acols = AS * MB * arow;                             // TS: A buffers
   static constexpr int NS0 = (512 - acols) / per;
-  static constexpr int NS = NS0 >= 8 ? 8 : NS0;                            // TMEM score buffers
+  static constexpr int NS = NS0 >= KM_NS_MAX ? KM_NS_MAX : NS0;            // TMEM score buffers
   static constexpr uint32_t a_base = NS * per;                             // first A column (TS)
   static constexpr uint32_t cols = NS * per + acols;
   static constexpr uint32_t alloc = cols <= 32 ? 32 : cols <= 64 ? 64 : cols <= 128 ? 128 : cols <= 256 ? 256 : 512;
@@ -666,7 +662,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   // A operand in TMEM (written by the transform with tcgen05.st, read by the MMA): takes the A
   // tile off shared memory (its stores and the MMA's operand reads) where the columns fit
   constexpr bool TS = tc_a_in_tmem<KP, TR>();
-  constexpr bool K3 = TS;  // one score column per centre (see TcTmem)
+  // one score column per centre (see TcTmem): the tail MMA xh·wl re-reads the xh k-steps of A —
+  // from TMEM (TS) or from the SW128 shared-memory tile — into the same accumulator
+  constexpr bool K3 = KM_K3_SMEM || TS;
   using TM = TcTmem<KP, MB, TcLayout<MP>::HW, TS ? TcStages<MP, KP>::a : 0, K3>;
   constexpr int SC = K3 ? KP : 2 * KP;  // score columns per M block
   // Active epilogue groups.  A group waiting on tile g must know that the previous fill of the
@@ -707,18 +705,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   const int km = k * m;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t ntiles = (a.n + TR - 1) / TR;
-  // Tiles [0, ntiles − D) in one contiguous range per CTA, [t_lo, t_lo + my_tiles) (TLB- and
-  // DRAM-page-friendly streams); the last D (resident: a.pool_tiles) go to whichever CTA asks
-  // first.  Ring position g carries its tile id in s_tile[g % 64] (producer → consumers, published
-  // by the full-barrier arrive); after the last tile of a pass the producer emits 3 sentinels
-  // (id −(g_end + 1)) that flow through every role like empty tiles, so each transform / MMA /
-  // epilogue group (strides 2, 2, 3) meets one and knows the pass ended.
-  const int64_t pool_n = resident ? a.pool_tiles : 0;
-  const int64_t nstatic = ntiles - pool_n;
-  const int64_t t_lo = nstatic * blockIdx.x / gridDim.x;
-  const int my_tiles = (int)(nstatic * (blockIdx.x + 1) / gridDim.x - t_lo);
-  __shared__ long long s_tile[64];
-  __shared__ int s_next_g0;
+  // contiguous tile range per CTA: [t_lo, t_lo + my_tiles) (TLB- and DRAM-page-friendly streams)
+  const int64_t t_lo = ntiles * blockIdx.x / gridDim.x;
+  const int my_tiles = (int)(ntiles * (blockIdx.x + 1) / gridDim.x - t_lo);
   const int nacc = km + k;
   const int npre = resident ? min(RS, my_tiles) : 0;  // next-pass tiles streamed during the tail
 
@@ -792,7 +781,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   int cb = 0;      // resident: s_cbuf half holding C_t
   int g0 = 0;      // tiles of earlier passes (ring positions continue across passes)
   int issued = 0;  // producer: tiles of the current pass already in flight
-  int pre_g0 = 0;  // producer: ring position of the next pass's prefetched tiles
+  int last_pass_tiles = my_tiles;
 
   // tuning only: per-pass phase ends (globaltimer, max over CTAs) of the resident loop
   unsigned long long* pst = (KM_TC_TUNING && a.dbg_times != nullptr && resident && tid == 0)
@@ -800,11 +789,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   for (int it = 0;; ++it) {
     // tiles of this pass (resident skip_first: the labels and their sums come from a separate
     // first pass + cluster-sums launch, so iteration 0 starts at the tail with Δ = 0)
-    const bool skip_pass = resident && it == 0 && a.skip_first;
-    const int pass_tiles = skip_pass ? 0 : my_tiles;  // static tiles of this pass (+ pool tiles)
+    const int pass_tiles = (resident && it == 0 && a.skip_first) ? 0 : my_tiles;
+    last_pass_tiles = pass_tiles;
     const bool heavy = s_heavy != 0;
-    // tile id of ring position g (volatile: written by the producer between uses of the position)
-    auto tile_of = [&](int g) -> long long { return *reinterpret_cast<volatile long long*>(&s_tile[g & 63]); };
     const double* C = resident ? s_cbuf + cb * km : a.c64;
     if (pst && it < 256 && blockIdx.x == 0) pst[it * 8 + 0] = globaltimer();
     if (pst && (it == 100 || it == 101 || it == 150))
@@ -891,15 +878,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       // ===================== TMA producer: tile g → raw slot g % RS =====================
       if (lane == 0) {
         const uint64_t pol = l2_policy_evict_first();
-        auto issue = [&](int g, long long tile) {
+        auto issue = [&](int g, int i) {
           const int s = g % RS;
           if (g >= RS) mbar_wait(empty_raw + s, ((g / RS) - 1) & 1);
-          *reinterpret_cast<volatile long long*>(&s_tile[g & 63]) = tile;
-          if (tile < 0) {  // sentinel: completes the slot's phase without data
-            mbar_arrive(full_raw + s);
-            return;
-          }
-          const int64_t row0 = tile * TR;
+          const int64_t row0 = (t_lo + i) * TR;
           const int64_t rem = a.n - row0;
           const int rows = rem < TR ? (int)rem : TR;
           const uint32_t bytes = ((uint32_t)rows * m * 4u) & ~15u;
@@ -908,25 +890,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             bulk_g2s_hint(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes, full_raw + s,
                           pol);
         };
-        int i = issued;
-        for (; i < pass_tiles; ++i) issue(g0 + i, t_lo + i);
-        int next0 = g0;
-        if (!skip_pass) {
-          if (pool_n > 0) {  // the dynamic tail: tickets until the pool is empty
-            for (;;) {
-              const unsigned int t = atomicAdd(a.pool + (it % 3), 1u);
-              if ((int64_t)t >= pool_n) break;
-              issue(g0 + i, nstatic + (long long)t);
-              ++i;
-            }
-          }
-          const int gend = g0 + i;
-          for (int j = 0; j < 3; ++j) issue(gend + j, -(long long)gend - 1);
-          next0 = gend + 3;
-        }
-        s_next_g0 = next0;
-        pre_g0 = next0;
-        for (int j = 0; j < npre; ++j) issue(next0 + j, t_lo + j);  // next pass (resident)
+        for (int i = issued; i < pass_tiles; ++i) issue(g0 + i, i);
+        for (int j = 0; j < npre; ++j) issue(g0 + pass_tiles + j, j);  // next pass (resident)
       }
       issued = npre;
     } else if (warp >= kMmaWarp) {
@@ -938,7 +903,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       constexpr uint32_t idesc = idesc_f16(SC);
       const uint64_t bdescL = make_desc(w0 + KP * 128, 16, 1024);  // B rows KP.. ([wl | 0]) for the K3 tail
       const uint64_t bdesc0 = make_desc(w0, 16, 1024);
-      for (int i = (mj - (g0 & 1)) & 1; !skip_pass && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
+      for (int i = (mj - (g0 & 1)) & 1; i < pass_tiles && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
         const int g = g0 + i;
         const int sa = g % AS, ss = g % TM::NS;
         long long* ms = (KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && i < 64 && lane == 0 && it == (resident ? 100 : 0))
@@ -949,10 +914,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         if (g >= TM::NS) mbar_wait(s_empty + ss, ((g / TM::NS) - 1) & 1);
         if (ms) ms[2] = clock64();
         tc_fence_after();
-        const long long tile = tile_of(g);
         if (elect_one()) {
 #pragma unroll
-          for (int mb = 0; mb < (tile >= 0 ? MB : 0); ++mb) {  // block mb: points 128·mb.. of the tile → columns mb·2KP..
+          for (int mb = 0; mb < MB; ++mb) {  // block mb: points 128·mb.. of the tile → columns mb·2KP..
             const uint32_t dcol = tm + ss * TM::per + mb * SC;
             if constexpr (TS) {  // A from TMEM: 16 halfs = 8 columns per k-step
               const uint32_t at = tm + TM::a_base + (uint32_t)(sa * TM::arow);
@@ -969,15 +933,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
 #pragma unroll
               for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
                 mma_f16(dcol, adesc0 + 2 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+              if constexpr (K3) {
+#pragma unroll
+                for (int ks = 0; ks < TM::ktail; ++ks)  // + xh · wl (the xh k-steps again), same accumulator
+                  mma_f16(dcol, adesc0 + 2 * ks, bdescL + 2 * ks, idesc, 1u);
+              }
             }
           }
-          // (a sentinel commits too: the arrive then still follows every earlier MMA of this thread)
           mma_commit(s_full + ss);   // scores ready
           mma_commit(a_empty + sa);  // A buffer consumed
         }
         __syncwarp();
         if (ms) ms[3] = clock64();
-        if (tile < 0 && g + kMmaWarps >= (int)(-tile - 1) + 3) break;  // past the last sentinel of this warp
       }
     } else if (warp < kTransformWarps) {
       // ===================== transform: thread = point; group tg takes tiles g ≡ tg (mod 2) =====================
@@ -986,28 +953,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
       const int key = p & 7;
       const float* __restrict__ gx = a.x;
-      for (int i = ((tg - g0) % kTransformGroups + kTransformGroups) % kTransformGroups; !skip_pass;
+      for (int i = ((tg - g0) % kTransformGroups + kTransformGroups) % kTransformGroups; i < pass_tiles;
            i += kTransformGroups) {
         const int g = g0 + i;
         const int s = g % RS, sa = g % AS;
-        mbar_wait(full_raw + s, (g / RS) & 1);
-        const long long tile = tile_of(g);
-        if (tile < 0) {  // sentinel: an empty tile through the A ring (keeps every barrier's phases)
-          if (g >= AS && !(KM_DBG_FLAGS & 4)) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(empty_raw + s);
-            if (!(KM_DBG_FLAGS & 4)) mbar_arrive(a_full + sa);
-          }
-          if (g + kTransformGroups >= (int)(-tile - 1) + 3) break;
-          continue;
-        }
-        const int64_t row0 = tile * TR;
+        const int64_t row0 = (t_lo + i) * TR;
         const int64_t rem = a.n - row0;
         const int rows = rem < TR ? (int)rem : TR;
         const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
         long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
         if (stamp) ts[0] = clock64();
+        if (KM_GROUP_WAIT & 2) {  // one warp of the group polls both barriers, the other three park in bar.sync
+          if ((warp & 3) == 0) {
+            mbar_wait(full_raw + s, (g / RS) & 1);
+            if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+          }
+          named_bar_sync(1 + kEpiGroups + tg, 128);
+          tc_fence_after();
+        } else {
+          mbar_wait(full_raw + s, (g / RS) & 1);
+        }
         if (stamp) ts[1] = clock64();
         if (KM_DBG_FLAGS & 4) {  // tuning only: measure the TMA stream alone
           __syncwarp();
@@ -1015,7 +980,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           continue;
         }
         const float* rs = raw + s * (S.raw_stride / 4);
-        if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+        if (!(KM_GROUP_WAIT & 2) && g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
         if (stamp) ts[7] = clock64();
         unsigned char* s_a = sm + S.off_a + sa * (TR * 128);
 #pragma unroll
@@ -1101,16 +1066,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const double scale_d = a.scale_d;
       const bool use_dscale = a.use_dscale != 0, exact_only = a.exact_only != 0;
       unsigned int my_changed = 0, my_rechecked = 0;
-      // previous label of point p + 128·mb of the i-th tile of the pass (or -1): static tiles are
-      // prefetched two tiles of this group ahead; pool tiles (-2) load when they arrive
-      auto prev_label = [&](int i, int mb) -> int {
-        if (full) return -1;
-        if (i >= pass_tiles) return -2;
+      auto prev_label = [&](int i, int mb) -> int {  // previous label of point p + 128·mb of tile i (or -1)
+        if (full || i >= pass_tiles) return -1;
         if (KM_DBG_FLAGS & 128) return 0;  // timing experiment only: no label loads
         const int64_t r = (t_lo + i) * TR + 128 * mb + p;
         return r < a.n ? __ldcg(a.labels + r) : -1;  // written by this CTA in the previous pass
       };
-      const int i0 = ((e - g0) % EG + EG) % EG;  // groups ≥ EG idle
+      const int i0 = e < EG ? ((e - g0) % EG + EG) % EG : pass_tiles;  // groups ≥ EG idle
       // previous labels prefetched two tiles of this group ahead (an L2 or DRAM round trip
       // must not stall the epilogue)
       int old_n1[MB], old_n2[MB];
@@ -1119,9 +1081,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         old_n1[mb] = prev_label(i0, mb);
         old_n2[mb] = prev_label(i0 + EG, mb);
       }
-      for (int i = i0; e < EG && !skip_pass && !(KM_DBG_FLAGS & 4); i += EG) {
+      for (int i = i0; i < pass_tiles && !(KM_DBG_FLAGS & 4); i += EG) {
         const int g = g0 + i;
         const int ss = g % TM::NS;
+        const int64_t row0 = (t_lo + i) * TR;
+        const int64_t rem = a.n - row0;
+        const int rows = rem < TR ? (int)rem : TR;
         int olds[MB];
 #pragma unroll
         for (int mb = 0; mb < MB; ++mb) {
@@ -1140,20 +1105,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         }
         if (stamp) ts[5] = clock64();
         tc_fence_after();
-        const long long tile = tile_of(g);
-        if (tile < 0) {  // sentinel
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_empty + ss);
-          if (g + EG >= (int)(-tile - 1) + 3) break;
-          continue;
-        }
-        const int64_t row0 = tile * TR;
-        const int64_t rem = a.n - row0;
-        const int rows = rem < TR ? (int)rem : TR;
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb)
-          if (olds[mb] == -2) olds[mb] = (128 * mb + p < rows) ? __ldcg(a.labels + row0 + 128 * mb + p) : -1;
         if (KM_DBG_FLAGS & 32) {  // timing experiment only: no epilogue work (labels unchanged)
           tc_fence_before();
           __syncwarp();
@@ -1325,8 +1276,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     // ===================== tail (all warps) =====================
     tc_fence_before();
     __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
-    if (tid == 0 && !skip_pass) {  // the next pass is heavy if this one changed > 1/256 of the CTA's points
-      s_heavy = KM_HEAVY_PASSES && !no_sums && s_pass_changes * 256u > (unsigned int)my_tiles * kTileRows ? 1 : 0;
+    if (tid == 0 && pass_tiles > 0) {  // the next pass is heavy if this one changed > 1/256 of the CTA's points
+      s_heavy = KM_HEAVY_PASSES && !no_sums && s_pass_changes * 256u > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
       s_pass_changes = 0u;
     }
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
@@ -1379,7 +1330,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (blockIdx.x == 0) {
       unsigned long long* nxt = a.dlt + (size_t)((it + 1) % 3) * nacc;
       for (int i = tid; i < nacc; i += kThreadsTC) nxt[i] = 0ull;
-      if (tid == 0 && a.pool) a.pool[(it + 1) % 3] = 0u;  // the pool ticket of pass it + 1 (last used in pass it − 2)
     }
     // grid barrier (the cooperative-groups pattern): the CTA's writes are ordered before thread
     // 0's gpu-scope fence by the CTA barrier, so one fence per CTA (not one per thread) releases them
@@ -1450,7 +1400,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     // ---- resident finish (every CTA; CTA 0 publishes) — engine._finish_update / converged ----
     const bool pub = blockIdx.x == 0;
     bool stop = false;
-    if (pub && tid == 0 && !skip_pass) st->passes += 1;
+    if (pub && tid == 0 && pass_tiles > 0) st->passes += 1;
     if (exhausted) {
       // the final assign pass of an exhausted run: counts = bincount(L_T), C_T unchanged
       if (pub) {
@@ -1561,13 +1511,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     __syncthreads();
     if (pst && it < 256) atomicMax(pst + it * 8 + 7, globaltimer());
     if (stop) break;
-    g0 = s_next_g0;  // the ring position after this pass's tiles and sentinels (set by the producer)
+    g0 += pass_tiles;
   }
   // ---- teardown ----
   if (resident && warp == kProducerWarp && lane == 0) {
     // the prefetched tiles of the pass that does not run: let their copies land before exit
     for (int j = 0; j < npre; ++j) {
-      const int g = pre_g0 + j;
+      const int g = g0 + last_pass_tiles + j;
       mbar_wait(full_raw + g % RS, (g / RS) & 1);
     }
   }

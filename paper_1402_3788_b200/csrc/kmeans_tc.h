@@ -44,12 +44,6 @@ struct TcArgs {
   FinishArgs fin;
   int32_t resident;        // 1: run the whole loop in this (cooperative) launch, see lloyd_pass_tc_kernel
   unsigned int* grid_sync; // resident: [0] barrier arrivals (zeroed before the launch)
-  // Dynamic tail (resident): the last `pool_tiles` tiles of every pass are handed out by an atomic
-  // ticket (pool[pass % 3], rotated and cleared like the deltas) to whichever CTA runs out of its
-  // static range first — the per-CTA pass time varies by ~10% from pass to pass (data-dependent),
-  // and the grid barrier waits for the slowest CTA.
-  unsigned int* pool;
-  int64_t pool_tiles;
   unsigned long long* dlt; // resident: [3][k·m + k] per-pass deltas (zeroed before the launch)
   // Row-sharded multi-GPU resident loop: after its local grid barrier every rank pushes its Δ
   // into every rank's exchange buffer over NVLink peer memory (CUDA IPC mappings) and sums the
