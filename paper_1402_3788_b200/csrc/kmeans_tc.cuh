@@ -988,7 +988,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           const int pp = p + 128 * mb;
           const bool active = pp < rows;
           float xs[L::HW];
-          if (rows == TR) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
+          if (KM_DBG_FLAGS & 512) {  // timing experiment only: no raw-tile loads
+#pragma unroll
+            for (int f = 0; f < L::HW; ++f) xs[f] = 0.f;
+          } else if (rows == TR) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
             const float* xr = rs + pp * m;
 #pragma unroll
             for (int f = 0; f < L::HW; ++f) {
@@ -1013,6 +1016,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           uint32_t hw[L::HW / 2], lw[L::HW / 2];
 #pragma unroll
           for (int q = 0; q < L::HW / 2; ++q) {
+            if (KM_DBG_FLAGS & 512) {  // timing experiment only: no transform arithmetic
+              hw[q] = lw[q] = 0u;
+              continue;
+            }
             const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
             const float2 hf = __half22float2(h2);
             // x − fl(xh) for both lanes in one packed FADD2
@@ -1180,8 +1187,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             }
             mk[(ch * 16) >> 5] |= bits << ((ch * 16) & 31);
           }
-          int bi = (int)(cnt >> 8);
-          const bool unc = active && (cnt & 0xff) != 1u && !(KM_DBG_FLAGS & 256);  // (dbg 256: timing only)
+          int bi = (KM_DBG_FLAGS & 512) ? old : (int)(cnt >> 8);  // (dbg 512: timing only, labels frozen)
+          const bool unc = active && (cnt & 0xff) != 1u && !(KM_DBG_FLAGS & (256 | 512));  // (dbg 256: timing only)
           if (__any_sync(0xffffffffu, unc)) {
             if (unc) {
               if constexpr (KEEP) {  // the candidate mask (uncertified points only)
