@@ -8,6 +8,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -103,6 +104,7 @@ struct km_engine {
   bool full_first_pass = false;     // KM_FULL_FIRST_PASS=1: fused full first pass (epilogue atomics)
   bool no_resident = false;         // KM_NO_RESIDENT=1: launch-per-iteration loop
   bool sums_owner = false;          // KM_SUMS_OWNER=1: cluster-owner sums kernel (A/B)
+  bool call_trace = false;          // KM_CALL_TRACE=1: per-step device/host times of km_lloyd (stderr)
   int dbg_flags = 0;                // KM_TC_DBG
   const char* times_path = nullptr; // KM_TC_TIMES
   size_t sums_key = 0;              // cluster-sums launch geometry cache
@@ -929,6 +931,7 @@ int km_create(int32_t device, km_engine** out) {
   e->full_first_pass = getenv("KM_FULL_FIRST_PASS") && atoi(getenv("KM_FULL_FIRST_PASS")) != 0;
   e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
   e->sums_owner = getenv("KM_SUMS_OWNER") != nullptr;
+  e->call_trace = getenv("KM_CALL_TRACE") != nullptr;
   e->dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
   e->times_path = getenv("KM_TC_TIMES");
   e->num_sms = prop.multiProcessorCount;
@@ -1186,6 +1189,17 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
   double* pin_c0 = reinterpret_cast<double*>(e->pin);
   double* pin_c = pin_c0 + km;
   long long* pin_n = reinterpret_cast<long long*>(pin_c + km);
+  // KM_CALL_TRACE: device (events) and host (clock) time of each step of the call, on stderr
+  cudaEvent_t tev[6] = {};
+  double th[6] = {};
+  int nt = 0;
+  auto trace = [&]() {
+    if (!e->call_trace || nt >= 6) return;
+    if (!tev[nt]) cudaEventCreate(&tev[nt]);
+    cudaEventRecord(tev[nt], e->stream);
+    th[nt++] = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+  };
+  trace();
   if (!resume) {
     std::memcpy(pin_c0, c0, 8 * km);
     CK(cudaMemcpyAsync(e->cur, pin_c0, 8 * km, cudaMemcpyHostToDevice, e->stream));
@@ -1219,10 +1233,14 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
     const int passes_before = first ? 0 : hs->passes;  // (the begin kernel zeroed the device state)
     const bool skip = split && first;
     if (skip) {
+      trace();
       if ((r = launch_tc(e, true, false, false, false, true))) return r;  // labels of C0 only
+      trace();
       if ((r = launch_sums(e, e->tot))) return r;
+      trace();
     }
     if ((r = launch_tc(e, full, true, false, true, false, skip))) return r;
+    trace();
     if (e->profiling) CK(cudaEventRecord(ev1, e->stream));
     // one round trip: state + (if the loop is done) the model
     CK(cudaMemcpyAsync(hs, e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
@@ -1230,6 +1248,18 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
     CK(cudaMemcpyAsync(pin_n, e->model_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
     CK(cudaStreamSynchronize(e->stream));
     e->stats.host_syncs += 1;
+    if (e->call_trace && nt > 1) {
+      const double t_end = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+      fprintf(stderr, "km_lloyd trace (device us | host us): ");
+      for (int i = 1; i < nt; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[i - 1], tev[i]);
+        fprintf(stderr, "[%d] %.1f | %.1f  ", i, ms * 1e3, th[i] - th[i - 1]);
+      }
+      fprintf(stderr, "sync wait %.1f\n", t_end - th[nt - 1]);
+      for (int i = 0; i < nt; ++i) cudaEventDestroy(tev[i]);
+      nt = 6;
+    }
     const DevState s = *hs;
     const int ran = s.passes - passes_before + (skip ? 1 : 0);
     if (e->profiling && ran > 0) {

@@ -83,6 +83,23 @@ constexpr int kThreadsTC = (kRecheckWarp + 1) * 32;
 template <int KP, int TR>
 __host__ __device__ constexpr bool tc_a_in_tmem() { return KM_A_IN_TMEM && KP <= 32 && TR == 128; }
 
+// Per-epilogue-warp private Δ accumulators (plain shared-memory adds, no atomics: the shared atomic
+// unit takes ~5 lane-ops per clock per SM, which bounded the change-heavy passes) where the 12
+// copies fit in 56 KB; the recheck warp and the tail keep the CTA-shared atomic accumulator.
+#ifndef KM_PRIV_DELTA
+#define KM_PRIV_DELTA 1
+#endif
+template <int MP, int KP>
+__host__ __device__ constexpr int tc_pdelta_stride() { return KP * (MP + 1) + KP; }  // int64 entries per copy
+template <int MP, int KP>
+__host__ __device__ constexpr bool tc_pdelta() {
+  return KM_PRIV_DELTA && kEpiWarps * tc_pdelta_stride<MP, KP>() * 8 <= 56 * 1024;
+}
+template <int MP, int KP>
+__host__ __device__ constexpr int tc_pdelta_bytes() {
+  return tc_pdelta<MP, KP>() ? (kEpiWarps * tc_pdelta_stride<MP, KP>() * 8 + 1023) / 1024 * 1024 : 0;
+}
+
 template <int MP, int KP, int TR>
 struct TcBudget {
 #ifndef KM_TS_ABUF
@@ -95,7 +112,8 @@ struct TcBudget {
   static constexpr int fixed = (tc_a_in_tmem<KP, TR>() ? 0 : a * TR * 128) + 2 * KP * 128 +  // A ring, B tile
                                ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024 +       // Δ accumulators
                                kQueueCap * (8 + 4 * mw) + 1024 +                       // recheck queue
-                               2048 + 1024 + 8192;                                     // barriers, align, static
+                               2048 + 1024 + 8192 +                                    // barriers, align, static
+                               tc_pdelta_bytes<MP, KP>();                              // per-warp private Δ
   static constexpr int cres = ((3 * KP * MP + KP) * 8 + 1023) / 1024 * 1024;          // resident centres + totals
   // keep room for the resident loop's centres unless that would starve the raw ring
   // (the widest shapes then run launch-per-iteration)
@@ -429,7 +447,7 @@ struct TcTmem {
 template <int MP, int KP>
 struct TcSmem {
   static constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
-  uint32_t raw_stride, off_raw, off_a, off_w, off_acc, off_q, off_c, off_bar, total;
+  uint32_t raw_stride, off_raw, off_a, off_w, off_acc, off_pacc, off_q, off_c, off_bar, total;
   // kres = k for the resident loop (two fp64 centre sets stay in shared memory), else 0
   __host__ __device__ TcSmem(int m, int kres) {
     // fixed-size sections first (compile-time offsets: no per-use address arithmetic in the
@@ -438,7 +456,8 @@ struct TcSmem {
     off_w = 1024;                             // [2KP rows × 128 B] B operand (SW128)
     off_a = off_w + 2 * KP * 128;             // [AS][TR rows × 128 B]
     off_acc = off_a + (tc_a_in_tmem<KP, TcStages<MP, KP>::TR>() ? 0 : AS * TcStages<MP, KP>::TR * 128);                    // [KP·(MP+1) + KP] int64 Δ
-    off_q = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;    // recheck queue: rows, masks, scalars
+    off_pacc = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // [kEpiWarps][stride] private Δ
+    off_q = off_pacc + tc_pdelta_bytes<MP, KP>();                            // recheck queue: rows, masks, scalars
     off_raw = off_q + ((kQueueCap * (8 + 4 * ((KP + 31) / 32)) + 1024) + 1023) / 1024 * 1024;
     // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
     raw_stride = ((uint32_t)TcStages<MP, KP>::TR * m * 4 + 256 + 1023) & ~1023u;
@@ -575,7 +594,11 @@ __device__ __forceinline__ int exact_candidates(const float* __restrict__ gx, in
 //    atomics.
 static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int m, int64_t wrow0, int lane, int bi, int old,
                                         unsigned int pend, bool full, unsigned long long* s_acc, int km,
-                                        float scale_f, double scale_d, bool use_dscale) {
+                                        float scale_f, double scale_d, bool use_dscale, bool priv) {
+  // priv: s_acc is this warp's private accumulator — the lane-per-feature path adds without atomics
+  auto add = [&](unsigned long long* p, unsigned long long v) {
+    if (priv) *p += v; else smem_add64(p, v);
+  };
   auto fixed = [&](float xv) -> long long {
     return use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d)) : __float2ll_rn(__fmul_rn(xv, scale_f));
   };
@@ -616,11 +639,11 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int 
       const int nb = __shfl_sync(0xffffffffu, bi, src[j]), ob = __shfl_sync(0xffffffffu, old, src[j]);
       if (lane < m) {
         const long long v = fixed(xv[j]);
-        smem_add64(s_acc + (size_t)nb * m + lane, (unsigned long long)v);
-        if (ob >= 0) smem_add64(s_acc + (size_t)ob * m + lane, (unsigned long long)(-v));
+        add(s_acc + (size_t)nb * m + lane, (unsigned long long)v);
+        if (ob >= 0) add(s_acc + (size_t)ob * m + lane, (unsigned long long)(-v));
       } else if (lane == m) {
-        smem_add64(s_acc + (size_t)km + nb, 1ull);
-        if (ob >= 0) smem_add64(s_acc + (size_t)km + ob, ~0ull);
+        add(s_acc + (size_t)km + nb, 1ull);
+        if (ob >= 0) add(s_acc + (size_t)km + ob, ~0ull);
       }
     }
   }
@@ -633,7 +656,11 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int 
 static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__ rs, uint32_t bulk_elems,
                                                        const float* __restrict__ gx_tile, int m, int prow0, int lane,
                                                        int bi, int old, unsigned int pend, unsigned long long* s_acc,
-                                                       int km, float scale_f, double scale_d, bool use_dscale) {
+                                                       int km, float scale_f, double scale_d, bool use_dscale,
+                                                       bool priv) {
+  auto add = [&](unsigned long long* p, unsigned long long v) {
+    if (priv) *p += v; else smem_add64(p, v);
+  };
   while (pend) {
     const int j = __ffs(pend) - 1;
     pend &= pend - 1;
@@ -642,11 +669,11 @@ static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__
       const uint32_t e = (uint32_t)(prow0 + j) * m + lane;
       const float v = e < bulk_elems ? rs[e] : __ldg(gx_tile + e);
       const long long q = use_dscale ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f));
-      smem_add64(s_acc + (size_t)nb * m + lane, (unsigned long long)q);
-      if (ob >= 0) smem_add64(s_acc + (size_t)ob * m + lane, (unsigned long long)(-q));
+      add(s_acc + (size_t)nb * m + lane, (unsigned long long)q);
+      if (ob >= 0) add(s_acc + (size_t)ob * m + lane, (unsigned long long)(-q));
     } else if (lane == m) {
-      smem_add64(s_acc + (size_t)km + nb, 1ull);
-      if (ob >= 0) smem_add64(s_acc + (size_t)km + ob, ~0ull);
+      add(s_acc + (size_t)km + nb, 1ull);
+      if (ob >= 0) add(s_acc + (size_t)km + ob, ~0ull);
     }
   }
 }
@@ -684,6 +711,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   float* raw = reinterpret_cast<float*>(sm + S.off_raw);
   unsigned char* s_w = sm + S.off_w;
   unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(sm + S.off_acc);
+  constexpr bool PD = tc_pdelta<MP, KP>();
+  constexpr int PST = tc_pdelta_stride<MP, KP>();
+  unsigned long long* s_pacc = reinterpret_cast<unsigned long long*>(sm + S.off_pacc);
   constexpr int MW = (KP + 31) / 32;                                          // candidate mask words
   long long* s_q = reinterpret_cast<long long*>(sm + S.off_q);                 // [cap] row << 8 | old + 1
   uint32_t* s_qm = reinterpret_cast<uint32_t*>(sm + S.off_q + kQueueCap * 8);  // [cap][MW] candidate masks
@@ -740,6 +770,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       for (int i = tid; i < AS * TR * 8; i += nthr)
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
     for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
+    if (PD)
+      for (int i = tid; i < kEpiWarps * PST; i += nthr) s_pacc[i] = 0ull;
     for (int i = tid; i < kQueueCap; i += nthr) s_q[i] = 0;
     if (resident) {
       for (int i = tid; i < km; i += nthr) s_cbuf[i] = a.c64[i];
@@ -1249,13 +1281,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           }
           const unsigned int pend = __ballot_sync(0xffffffffu, chg && !no_sums);
           if (pend) {
+            unsigned long long* my_acc = PD ? s_pacc + ew * PST : s_acc;  // this warp's (private) Δ
             if (heavy)
               delta_rows_smem(raw + (g % RS) * (S.raw_stride / 4), (((uint32_t)rows * m * 4u) & ~15u) >> 2,
-                              a.x + row0 * m, m, 128 * mb + (p & ~31), lane, bi, old, pend, s_acc, km, scale_f,
-                              scale_d, use_dscale);
+                              a.x + row0 * m, m, 128 * mb + (p & ~31), lane, bi, old, pend, my_acc, km, scale_f,
+                              scale_d, use_dscale, PD);
             else
-              delta_rows(a.x, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, s_acc, km, scale_f, scale_d,
-                         use_dscale);
+              delta_rows(a.x, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, my_acc, km, scale_f, scale_d,
+                         use_dscale, PD);
           }
         }
         if (heavy) {  // the raw tile's rows are no longer needed: the TMA producer may refill it
@@ -1297,6 +1330,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
       for (unsigned int q = s_qn[2] + tid; q < qn; q += kThreadsTC) redecide(q, s_q[q]);
       __syncthreads();
+      if (PD) {  // the epilogue warps' private Δ into the CTA's accumulator (and cleared for the next pass)
+        for (int i = tid; i < nacc; i += kThreadsTC) {
+          unsigned long long v = 0ull;
+#pragma unroll 4
+          for (int w = 0; w < kEpiWarps; ++w) {
+            v += s_pacc[w * PST + i];
+            s_pacc[w * PST + i] = 0ull;
+          }
+          s_acc[i] += v;
+        }
+        __syncthreads();
+      }
       if (tid == 0) {
         s_qn[0] = 0u;
         s_qn[1] = 0u;

@@ -8,7 +8,7 @@
 #include <cstdint>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
-constexpr int ITERS = 4096, K = 16, M = 25, WARPS = 12;
+constexpr int ITERS = 4096, K = 16, M = 25, WARPS = 6;
 
 __device__ __forceinline__ void add64_pair(unsigned long long* addr, unsigned long long v) {
   unsigned int* p = reinterpret_cast<unsigned int*>(addr);
@@ -19,8 +19,8 @@ __device__ __forceinline__ void add64_pair(unsigned long long* addr, unsigned lo
 
 template <int MODE>
 __global__ void __launch_bounds__(WARPS * 32, 1) k_acc(unsigned long long* out, unsigned seed) {
-  __shared__ unsigned long long acc[WARPS][K * (M + 1)];
-  for (int i = threadIdx.x; i < WARPS * K * (M + 1); i += blockDim.x) (&acc[0][0])[i] = 0;
+  __shared__ unsigned long long acc[WARPS][K * (M + 1) * 2];
+  for (int i = threadIdx.x; i < WARPS * K * (M + 1) * 2; i += blockDim.x) (&acc[0][0])[i] = 0;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned s = seed ^ (blockIdx.x * 7919u + warp * 104729u);
@@ -34,12 +34,20 @@ __global__ void __launch_bounds__(WARPS * 32, 1) k_acc(unsigned long long* out, 
       if (MODE == 0) add64_pair(dst, v);
       else if (MODE == 1) atomicAdd(dst, v);
       else if (MODE == 2) asm volatile("red.shared.add.u64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(v) : "memory");
+      else if (MODE == 4) {  // four 16-bit limbs, 32-bit reductions without return
+        unsigned* d32 = reinterpret_cast<unsigned*>(mine) + 4 * (L * (M + 1) + lane);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(d32);
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sa), "r"((unsigned)(v & 0xffff)) : "memory");
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sa + 4), "r"((unsigned)((v >> 16) & 0xffff)) : "memory");
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sa + 8), "r"((unsigned)((v >> 32) & 0xffff)) : "memory");
+        asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(sa + 12), "r"((unsigned)((long long)v >> 48)) : "memory");
+      }
       else *dst += v;
     }
   }
   __syncthreads();
   unsigned long long t = 0;
-  for (int i = threadIdx.x; i < WARPS * K * (M + 1); i += blockDim.x) t += (&acc[0][0])[i];
+  for (int i = threadIdx.x; i < WARPS * K * (M + 1) * 2; i += blockDim.x) t += (&acc[0][0])[i];
   atomicAdd(out, t);
 }
 
@@ -72,5 +80,6 @@ int main() {
   run<1>("atomicAdd u64 (shared)", sms);
   run<2>("red.shared.add.u64", sms);
   run<3>("warp-private LDS/STS", sms);
+  run<4>("4x red.shared.add.u32 (limbs)", sms);
   return 0;
 }
