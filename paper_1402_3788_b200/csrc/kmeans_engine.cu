@@ -105,6 +105,7 @@ struct km_engine {
   bool no_resident = false;         // KM_NO_RESIDENT=1: launch-per-iteration loop
   bool sums_owner = false;          // KM_SUMS_OWNER=1: cluster-owner sums kernel (A/B)
   bool call_trace = false;          // KM_CALL_TRACE=1: per-step device/host times of km_lloyd (stderr)
+  bool no_big_k = false;            // KM_NO_BIG_K=1: K > 128 takes the SIMT blocked pass (A/B)
   int dbg_flags = 0;                // KM_TC_DBG
   const char* times_path = nullptr; // KM_TC_TIMES
   size_t sums_key = 0;              // cluster-sums launch geometry cache
@@ -286,18 +287,22 @@ static int launch_blocked_mp(km_engine* e, const PassArgs& a, size_t smem, int m
 // tensor-core path: fp32 resident points, m ≤ 31 ([xh|xl] + the ones column fit one 128-byte
 // fp16 row), k ≤ 128 (N = 2·KP ≤ 256 per MMA; 2 warpgroups × 2·KP TMEM columns ≤ 512)
 static bool tc_eligible(const km_engine* e) {
-  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= 128;
+  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= (e->no_big_k ? 128 : 512);
 }
 static bool use_tc(const km_engine* e) { return e->path_pref != 1 && e->path_pref != 3 && tc_eligible(e); }
 
 static int tc_mp_for(int m) { return m <= 7 ? 7 : m <= 15 ? 15 : m <= 23 ? 23 : 31; }
 
 static float host_err_coef_tc(int m, int mp) {
-  // |S_tc − S| ≤ coef·(‖x‖ + max‖c‖)²: FMA-chain/alignment error of the 3·KS tf32
-  // MMA steps + the dropped Xl·Wl term + tf32 truncation of the lo parts + the
-  // fp32 rounding of x, c, ‖c‖² + the reference's own fp64 rounding; ×2 safety.
-  // Measured worst case on B200 (tests/test_gpu_tensorcore.py): ≈ 6e-7 ≈ 10·2⁻²⁴ for every m;
-  // the coefficient below keeps ≥ 6× margin over it.
+  // |S_tc − S| ≤ coef·(‖x‖ + max‖c‖)² for the kind::f16 scores (fp16 hi/lo split of both
+  // operands, fp32 accumulation): the split residue (|x − xh − xl| ≤ 2⁻²²|x|, same for w) and the
+  // dropped xl·wl term (≤ 3·2⁻²¹ of Σ|x_f w_f| ≤ 2‖x‖‖c‖), the accumulation of the k-steps (the
+  // products are exact; each k-step's sum and the fp32 accumulator are charged 2⁻²³ of the
+  // largest product per step), the fp32 rounding of c and ‖c‖², and the reference's own fp64
+  // rounding.  The hardware adder's alignment width is not documented, so the coefficient is
+  // checked adversarially: tests/test_gpu_tensorcore.py sweeps product ratios 2⁻⁸ … 2⁻³⁰ with one
+  // large and 24 small same-sign (or alternating) products per k-step and requires the worst
+  // observed error ≤ coef/4 (profiles/r02_tensorcore_margins.txt has the margins).
   const int ks = (mp + 1 + 7) / 8;
   return (float)std::max((m + 8 + 12 * ks) * std::ldexp(1.0, -23), std::ldexp(1.0, -18));
 }
@@ -652,7 +657,8 @@ static int ensure_k(km_engine* e, int32_t k) {
   e->n_partials = grid_for(e, e->n);
   if ((r = grow(e, &e->partials, &e->partials_cap, sizeof(ArgMax) * (size_t)e->n_partials))) return r;
   if ((r = dalloc(e, &e->winner, sizeof(ArgMax)))) return r;
-  e->kp = k <= 64 ? ((k + 15) & ~15) : ((k + 31) & ~31);
+  // tensor-core N padding: 16s to 64, 32s to 128, then the large-K instantiations 256 / 512
+  e->kp = k <= 64 ? ((k + 15) & ~15) : k <= 128 ? ((k + 31) & ~31) : k <= 256 ? 256 : k <= 512 ? 512 : 1024;
   if ((r = dalloc(e, &e->wop, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp))) return r;
   CK(cudaMemsetAsync(e->wop, 0, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp, e->stream));
   if ((r = dalloc(e, &e->tot, 8 * ((size_t)k * m + k)))) return r;
@@ -932,6 +938,7 @@ int km_create(int32_t device, km_engine** out) {
   e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
   e->sums_owner = getenv("KM_SUMS_OWNER") != nullptr;
   e->call_trace = getenv("KM_CALL_TRACE") != nullptr;
+  e->no_big_k = getenv("KM_NO_BIG_K") != nullptr;
   e->dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
   e->times_path = getenv("KM_TC_TIMES");
   e->num_sms = prop.multiProcessorCount;

@@ -123,7 +123,7 @@ __device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, 
   // rounded up for the filter bound; then the SIMT operand w = −2·fl32(c) (zero padded) and the
   // tensor-core operand (fp16 hi/lo split of W~' = 2^s·(−2·fl32(c)), 2^2s·‖fl32(c)‖² at f = m):
   // row c < kp: [wh_c | wh_c], row kp + c: [wl_c | 0]  (hw halfs per part, 64-half rows)
-  __shared__ double s_cn2[128];  // tensor-core operand rows (kp ≤ 128)
+  __shared__ double s_cn2[512];  // tensor-core operand rows (kp ≤ 512)
   float local_max = 0.f;
   for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
     double s = 0.0;
@@ -131,7 +131,7 @@ __device__ __forceinline__ void block_prep_filter(const double* __restrict__ c, 
       const double v = (double)__double2float_rn(c[(size_t)cc * m + f]);
       s = __fma_rn(v, v, s);
     }
-    if (cc < 128) s_cn2[cc] = s;
+    if (cc < 512) s_cn2[cc] = s;
     cn[cc] = __double2float_rn(s);
     local_max = fmaxf(local_max, __double2float_ru(sqrt(s) * (1.0 + 1e-12)));
   }

@@ -45,6 +45,19 @@ namespace km {
 namespace tc {
 
 constexpr int kQueueCap = 768;                     // per-CTA staging of uncertified points (smem)
+// Large K (KP > 128, up to 512): the candidate masks grow to KP/32 words per queued point, so the
+// queue shrinks; the per-cluster Δ (K·M + K int64, 106 KB at K = 512) no longer fits shared memory
+// beside the 2·KP-row B operand and goes straight to global memory (native 64-bit atomics into the
+// pass's partial buffer, fire-and-forget).
+template <int KP>
+__host__ __device__ constexpr int tc_qcap() { return KP <= 128 ? kQueueCap : 128; }
+template <int KP>
+__host__ __device__ constexpr bool tc_gacc() { return KP > 128; }
+// 64-bit accumulate into the Δ accumulator: shared memory (two 32-bit atomics with carry) or, for
+// the large-K pass, global memory (one native atomic)
+__device__ __forceinline__ void acc_add64(unsigned long long* p, unsigned long long v) {
+  if (__isShared(p)) smem_add64(p, v); else atomicAdd(p, v);
+}
 constexpr long long kQueueFlag = 1ll << 62;
 // a queue entry of a point whose label CHANGED (not a recheck): flag | change | row << 16 |
 // (old + 1) << 8 | new.  The recheck warp applies its exact Δ off the epilogue's critical path.
@@ -106,12 +119,12 @@ struct TcBudget {
 #define KM_TS_ABUF 4
 #endif
   // A buffers: per transform group (a group owns buffers g mod a); in TMEM they are cheap
-  static constexpr int a = (tc_a_in_tmem<KP, TR>() ? KM_TS_ABUF : 2) * kTransformGroups;
+  static constexpr int a = (tc_a_in_tmem<KP, TR>() ? KM_TS_ABUF : KP > 128 ? 1 : 2) * kTransformGroups;
   static constexpr int mw = (KP + 31) / 32;
   static constexpr int raw_stride_max = ((TR * MP * 4 + 256 + 1023) / 1024) * 1024;
   static constexpr int fixed = (tc_a_in_tmem<KP, TR>() ? 0 : a * TR * 128) + 2 * KP * 128 +  // A ring, B tile
-                               ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024 +       // Δ accumulators
-                               kQueueCap * (8 + 4 * mw) + 1024 +                       // recheck queue
+                               (tc_gacc<KP>() ? 0 : ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024) +  // Δ accumulators
+                               tc_qcap<KP>() * (8 + 4 * mw) + 1024 +                   // recheck queue
                                2048 + 1024 + 8192 +                                    // barriers, align, static
                                tc_pdelta_bytes<MP, KP>();                              // per-warp private Δ
   static constexpr int cres = ((3 * KP * MP + KP) * 8 + 1023) / 1024 * 1024;          // resident centres + totals
@@ -456,9 +469,9 @@ struct TcSmem {
     off_w = 1024;                             // [2KP rows × 128 B] B operand (SW128)
     off_a = off_w + 2 * KP * 128;             // [AS][TR rows × 128 B]
     off_acc = off_a + (tc_a_in_tmem<KP, TcStages<MP, KP>::TR>() ? 0 : AS * TcStages<MP, KP>::TR * 128);                    // [KP·(MP+1) + KP] int64 Δ
-    off_pacc = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // [kEpiWarps][stride] private Δ
+    off_pacc = off_acc + (tc_gacc<KP>() ? 0 : ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024);  // [kEpiWarps][stride] private Δ
     off_q = off_pacc + tc_pdelta_bytes<MP, KP>();                            // recheck queue: rows, masks, scalars
-    off_raw = off_q + ((kQueueCap * (8 + 4 * ((KP + 31) / 32)) + 1024) + 1023) / 1024 * 1024;
+    off_raw = off_q + ((tc_qcap<KP>() * (8 + 4 * ((KP + 31) / 32)) + 1024) + 1023) / 1024 * 1024;
     // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
     raw_stride = ((uint32_t)TcStages<MP, KP>::TR * m * 4 + 256 + 1023) & ~1023u;
     off_c = off_raw + RS * raw_stride;        // resident: [2][kres·m] fp64 centres, then [kres·m + kres] int64 totals
@@ -485,7 +498,7 @@ __device__ __forceinline__ void grid_spin(const unsigned int* p, unsigned int ta
 // (kmeans_finish.cuh) writes to global memory for the launch-per-iteration path.
 __device__ __forceinline__ void cta_prep_operand(const double* __restrict__ C, int k, int m, int kp, float pre,
                                                  unsigned char* s_w, float* s_cmax) {
-  __shared__ double s_cn2[128];
+  __shared__ double s_cn2[512];  // tensor-core operand rows (kp ≤ 512)
   __shared__ float s_red[32];
   float local_max = 0.f;
   for (int cc = threadIdx.x; cc < k; cc += blockDim.x) {
@@ -597,7 +610,7 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int 
                                         float scale_f, double scale_d, bool use_dscale, bool priv) {
   // priv: s_acc is this warp's private accumulator — the lane-per-feature path adds without atomics
   auto add = [&](unsigned long long* p, unsigned long long v) {
-    if (priv) *p += v; else smem_add64(p, v);
+    if (priv) *p += v; else acc_add64(p, v);
   };
   auto fixed = [&](float xv) -> long long {
     return use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d)) : __float2ll_rn(__fmul_rn(xv, scale_f));
@@ -614,13 +627,13 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int 
       for (int j = 0; j < CH; ++j) {
         if (f0 + j < m) {
           const long long v = fixed(xv[j]);
-          smem_add64(s_acc + (size_t)bi * m + f0 + j, (unsigned long long)v);
-          if (old >= 0) smem_add64(s_acc + (size_t)old * m + f0 + j, (unsigned long long)(-v));
+          acc_add64(s_acc + (size_t)bi * m + f0 + j, (unsigned long long)v);
+          if (old >= 0) acc_add64(s_acc + (size_t)old * m + f0 + j, (unsigned long long)(-v));
         }
       }
     }
-    smem_add64(s_acc + (size_t)km + bi, 1ull);
-    if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+    acc_add64(s_acc + (size_t)km + bi, 1ull);
+    if (old >= 0) acc_add64(s_acc + (size_t)km + old, ~0ull);
     return;
   }
   while (pend) {
@@ -659,7 +672,7 @@ static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__
                                                        int km, float scale_f, double scale_d, bool use_dscale,
                                                        bool priv) {
   auto add = [&](unsigned long long* p, unsigned long long v) {
-    if (priv) *p += v; else smem_add64(p, v);
+    if (priv) *p += v; else acc_add64(p, v);
   };
   while (pend) {
     const int j = __ffs(pend) - 1;
@@ -700,7 +713,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   // after g − NS implies it (tcgen05.commit covers every earlier MMA of that thread).  So NS must
   // reach the first even multiple of EG; narrower score rings (KP > 32) run two groups and the
   // third idles.
-  constexpr int EG = TM::NS % 2 == 0 && TM::NS >= (kEpiGroups % 2 ? 2 * kEpiGroups : kEpiGroups) ? kEpiGroups : 2;
+  constexpr int EG = TM::NS < 2 ? 1
+                     : TM::NS % 2 == 0 && TM::NS >= (kEpiGroups % 2 ? 2 * kEpiGroups : kEpiGroups) ? kEpiGroups : 2;
   const bool resident = a.resident != 0;
   const TcSmem<MP, KP> S(MT > 0 ? MT : a.m, resident ? a.k : 0);
   constexpr int RS = TcStages<MP, KP>::raw, AS = TcStages<MP, KP>::a;
@@ -710,14 +724,16 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* raw = reinterpret_cast<float*>(sm + S.off_raw);
   unsigned char* s_w = sm + S.off_w;
-  unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(sm + S.off_acc);
-  constexpr bool PD = tc_pdelta<MP, KP>();
+  constexpr bool GACC = tc_gacc<KP>();
+  unsigned long long* s_acc = GACC ? a.part : reinterpret_cast<unsigned long long*>(sm + S.off_acc);
+  constexpr bool PD = tc_pdelta<MP, KP>() && !GACC;
   constexpr int PST = tc_pdelta_stride<MP, KP>();
   unsigned long long* s_pacc = reinterpret_cast<unsigned long long*>(sm + S.off_pacc);
   constexpr int MW = (KP + 31) / 32;                                          // candidate mask words
   long long* s_q = reinterpret_cast<long long*>(sm + S.off_q);                 // [cap] row << 8 | old + 1
-  uint32_t* s_qm = reinterpret_cast<uint32_t*>(sm + S.off_q + kQueueCap * 8);  // [cap][MW] candidate masks
-  unsigned int* s_qn = s_qm + kQueueCap * MW;                                  // [0] queue length
+  constexpr int QCAP = tc_qcap<KP>();
+  uint32_t* s_qm = reinterpret_cast<uint32_t*>(sm + S.off_q + QCAP * 8);  // [cap][MW] candidate masks
+  unsigned int* s_qn = s_qm + QCAP * MW;                                  // [0] queue length
   float* s_cmax = reinterpret_cast<float*>(s_qn + 4);                          // resident: max ‖c‖
   double* s_cbuf = reinterpret_cast<double*>(sm + S.off_c);                            // resident: [2][k·m]
   unsigned long long* s_tot = reinterpret_cast<unsigned long long*>(s_cbuf + 2 * (size_t)a.k * (MT > 0 ? MT : a.m));
@@ -769,10 +785,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (!TS)
       for (int i = tid; i < AS * TR * 8; i += nthr)
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
-    for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
+    if (!GACC)
+      for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
     if (PD)
       for (int i = tid; i < kEpiWarps * PST; i += nthr) s_pacc[i] = 0ull;
-    for (int i = tid; i < kQueueCap; i += nthr) s_q[i] = 0;
+    for (int i = tid; i < QCAP; i += nthr) s_q[i] = 0;
     if (resident) {
       for (int i = tid; i < km; i += nthr) s_cbuf[i] = a.c64[i];
       // totals of the current labels (peer loop after a separate first pass: the local sums in
@@ -843,12 +860,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
         if (f < m) {
           const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
                                            : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
-          smem_add64(s_acc + (size_t)nw * m + f, (unsigned long long)v);
-          if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
+          acc_add64(s_acc + (size_t)nw * m + f, (unsigned long long)v);
+          if (old >= 0) acc_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
         }
       }
-      smem_add64(s_acc + (size_t)km + nw, 1ull);
-      if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+      acc_add64(s_acc + (size_t)km + nw, 1ull);
+      if (old >= 0) acc_add64(s_acc + (size_t)km + old, ~0ull);
       s_q[q] = 0;  // free for the next pass
     };
     auto redecide = [&](unsigned int q, long long ent) {
@@ -870,12 +887,12 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           if (f < m) {
             const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
                                              : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
-            smem_add64(s_acc + (size_t)bl * m + f, (unsigned long long)v);
-            if (old >= 0) smem_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
+            acc_add64(s_acc + (size_t)bl * m + f, (unsigned long long)v);
+            if (old >= 0) acc_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
           }
         }
-        smem_add64(s_acc + (size_t)km + bl, 1ull);
-        if (old >= 0) smem_add64(s_acc + (size_t)km + old, ~0ull);
+        acc_add64(s_acc + (size_t)km + bl, 1ull);
+        if (old >= 0) acc_add64(s_acc + (size_t)km + old, ~0ull);
       }
       s_q[q] = 0;  // free for the next pass
     };
@@ -883,7 +900,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       // ===================== recheck warp: re-decides queued points while the pass streams =====================
       unsigned int done = 0;
       for (;;) {
-        const unsigned int avail = __shfl_sync(0xffffffffu, min(*reinterpret_cast<volatile unsigned int*>(s_qn), (unsigned int)kQueueCap), 0);
+        const unsigned int avail = __shfl_sync(0xffffffffu, min(*reinterpret_cast<volatile unsigned int*>(s_qn), (unsigned int)QCAP), 0);
         if (done < avail) {
           const unsigned int q = done + lane;
           if (q < avail) {
@@ -898,7 +915,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           const unsigned int fin = __shfl_sync(0xffffffffu, *reinterpret_cast<volatile unsigned int*>(s_qn + 1), 0);
           if (fin >= (unsigned int)kEpiWarps) {
             __threadfence_block();
-            const unsigned int av2 = __shfl_sync(0xffffffffu, min(*reinterpret_cast<volatile unsigned int*>(s_qn), (unsigned int)kQueueCap), 0);
+            const unsigned int av2 = __shfl_sync(0xffffffffu, min(*reinterpret_cast<volatile unsigned int*>(s_qn), (unsigned int)QCAP), 0);
             if (av2 == done) break;
           } else {
             __nanosleep(256);
@@ -932,7 +949,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const int mj = warp - kMmaWarp;
       const uint32_t a0 = smem_u32(sm + S.off_a), w0 = smem_u32(s_w);
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);  // warp-uniform → uniform registers
-      constexpr uint32_t idesc = idesc_f16(SC);
+      // N ≤ 256 per MMA: the large-K pass issues SC / 256 column blocks (B rows h·NN.. of each half)
+      constexpr int NSUB = SC > 256 ? SC / 256 : 1;
+      constexpr int NN = SC / NSUB;
+      constexpr uint32_t idesc = idesc_f16(NN);
       const uint64_t bdescL = make_desc(w0 + KP * 128, 16, 1024);  // B rows KP.. ([wl | 0]) for the K3 tail
       const uint64_t bdesc0 = make_desc(w0, 16, 1024);
       for (int i = (mj - (g0 & 1)) & 1; i < pass_tiles && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
@@ -963,12 +983,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             } else {
               const uint64_t adesc0 = make_desc(a0 + sa * (TR * 128) + mb * (128 * 128), 16, 1024);
 #pragma unroll
-              for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
-                mma_f16(dcol, adesc0 + 2 * ks, bdesc0 + 2 * ks, idesc, ks > 0 ? 1u : 0u);
-              if constexpr (K3) {
+              for (int h = 0; h < NSUB; ++h) {
+                const uint32_t dc = dcol + h * NN;
+                const uint64_t bo = (uint64_t)(h * NN * 128 / 16);  // B rows h·NN.. (address field, 16-B units)
 #pragma unroll
-                for (int ks = 0; ks < TM::ktail; ++ks)  // + xh · wl (the xh k-steps again), same accumulator
-                  mma_f16(dcol, adesc0 + 2 * ks, bdescL + 2 * ks, idesc, 1u);
+                for (int ks = 0; ks < L::KSTEPS; ++ks)  // +32 B per k-step = +2 in the descriptor's address field
+                  mma_f16(dc, adesc0 + 2 * ks, bdesc0 + bo + 2 * ks, idesc, ks > 0 ? 1u : 0u);
+                if constexpr (K3) {
+#pragma unroll
+                  for (int ks = 0; ks < TM::ktail; ++ks)  // + xh · wl (the xh k-steps again), same accumulator
+                    mma_f16(dc, adesc0 + 2 * ks, bdescL + bo + 2 * ks, idesc, 1u);
+                }
               }
             }
           }
@@ -1238,7 +1263,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
               // centre is strictly farther) — queue the point with its candidate mask
               ++my_rechecked;
               const unsigned int slot = atomicAdd(s_qn, 1u);
-              if (slot < kQueueCap) {
+              if (slot < QCAP) {
                 const float* gr = a.x + (row0 + pp) * m;  // keep the row in L2 until it is re-decided
                 prefetch_l2_keep(gr);
                 prefetch_l2_keep(gr + m - 1);
@@ -1273,7 +1298,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             // hand the Δ to the recheck warp (its loads and atomics leave the epilogue's critical
             // path); a full queue (rare) keeps it here
             const unsigned int slot = atomicAdd(s_qn, 1u);
-            if (slot < kQueueCap) {
+            if (slot < QCAP) {
               *reinterpret_cast<volatile long long*>(s_q + slot) =
                   kQueueFlag | kChangeFlag | ((row0 + 128 * mb + p) << 16) | ((long long)(old + 1) << 8) | bi;
               chg = false;
@@ -1327,7 +1352,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     const int stage_cap = (int)(RS * S.raw_stride / 8);
     {
       // queue entries the recheck warp had not reached when the pass ended: thread per point
-      const unsigned int qn = min(s_qn[0], (unsigned int)kQueueCap);
+      const unsigned int qn = min(s_qn[0], (unsigned int)QCAP);
       for (unsigned int q = s_qn[2] + tid; q < qn; q += kThreadsTC) redecide(q, s_q[q]);
       __syncthreads();
       if (PD) {  // the epilogue warps' private Δ into the CTA's accumulator (and cleared for the next pass)
@@ -1350,7 +1375,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       if (pst && it < 256) atomicMax(pst + it * 8 + 2, globaltimer());
     }
     if (!resident) {
-      for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
+      for (int i = tid; i < nacc && !GACC; i += kThreadsTC) {  // one flush of the CTA's Δ
         const unsigned long long v = s_acc[i];
         if (v) atomicAdd(a.part + i, v);
       }
