@@ -955,7 +955,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       constexpr uint32_t idesc = idesc_f16(NN);
       const uint64_t bdescL = make_desc(w0 + KP * 128, 16, 1024);  // B rows KP.. ([wl | 0]) for the K3 tail
       const uint64_t bdesc0 = make_desc(w0, 16, 1024);
-      for (int i = (mj - (g0 & 1)) & 1; i < pass_tiles && !(KM_DBG_FLAGS & 4); i += kMmaWarps) {
+      // Two issuers alternate tiles only when the score ring has an even depth: a buffer is then
+      // always reused by the same warp, whose own earlier wait orders the parity check.  With one
+      // score buffer (the K = 512 pass) consecutive tiles share it, and an issuer could pass the
+      // parity wait of a phase two behind — a single issuer takes every tile.
+      constexpr int NI = TM::NS % 2 == 0 ? kMmaWarps : 1;
+      for (int i = NI == 1 ? (mj == 0 ? 0 : pass_tiles) : (mj - (g0 & 1)) & 1; i < pass_tiles && !(KM_DBG_FLAGS & 4);
+           i += NI) {
         const int g = g0 + i;
         const int sa = g % AS, ss = g % TM::NS;
         long long* ms = (KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && i < 64 && lane == 0 && it == (resident ? 100 : 0))
