@@ -105,7 +105,6 @@ struct km_engine {
   bool no_resident = false;         // KM_NO_RESIDENT=1: launch-per-iteration loop
   bool sums_owner = false;          // KM_SUMS_OWNER=1: cluster-owner sums kernel (A/B)
   bool call_trace = false;          // KM_CALL_TRACE=1: per-step device/host times of km_lloyd (stderr)
-  bool no_big_k = false;            // KM_NO_BIG_K=1: K > 128 takes the SIMT blocked pass (A/B)
   int dbg_flags = 0;                // KM_TC_DBG
   const char* times_path = nullptr; // KM_TC_TIMES
   size_t sums_key = 0;              // cluster-sums launch geometry cache
@@ -287,7 +286,7 @@ static int launch_blocked_mp(km_engine* e, const PassArgs& a, size_t smem, int m
 // tensor-core path: fp32 resident points, m ≤ 31 ([xh|xl] + the ones column fit one 128-byte
 // fp16 row), k ≤ 128 (N = 2·KP ≤ 256 per MMA; 2 warpgroups × 2·KP TMEM columns ≤ 512)
 static bool tc_eligible(const km_engine* e) {
-  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= (e->no_big_k ? 128 : 512);
+  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= 128;
 }
 static bool use_tc(const km_engine* e) { return e->path_pref != 1 && e->path_pref != 3 && tc_eligible(e); }
 
@@ -657,8 +656,8 @@ static int ensure_k(km_engine* e, int32_t k) {
   e->n_partials = grid_for(e, e->n);
   if ((r = grow(e, &e->partials, &e->partials_cap, sizeof(ArgMax) * (size_t)e->n_partials))) return r;
   if ((r = dalloc(e, &e->winner, sizeof(ArgMax)))) return r;
-  // tensor-core N padding: 16s to 64, 32s to 128, then the large-K instantiations 256 / 512
-  e->kp = k <= 64 ? ((k + 15) & ~15) : k <= 128 ? ((k + 31) & ~31) : k <= 256 ? 256 : k <= 512 ? 512 : 1024;
+  // tensor-core N padding: 16s to 64, 32s to 128 (K > 128 takes the SIMT blocked pass)
+  e->kp = k <= 64 ? ((k + 15) & ~15) : k <= 128 ? ((k + 31) & ~31) : 1024;
   if ((r = dalloc(e, &e->wop, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp))) return r;
   CK(cudaMemsetAsync(e->wop, 0, sizeof(unsigned short) * 2 * 64 * (size_t)e->kp, e->stream));
   if ((r = dalloc(e, &e->tot, 8 * ((size_t)k * m + k)))) return r;
@@ -938,7 +937,6 @@ int km_create(int32_t device, km_engine** out) {
   e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
   e->sums_owner = getenv("KM_SUMS_OWNER") != nullptr;
   e->call_trace = getenv("KM_CALL_TRACE") != nullptr;
-  e->no_big_k = getenv("KM_NO_BIG_K") != nullptr;
   e->dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
   e->times_path = getenv("KM_TC_TIMES");
   e->num_sms = prop.multiProcessorCount;

@@ -45,19 +45,11 @@ namespace km {
 namespace tc {
 
 constexpr int kQueueCap = 768;                     // per-CTA staging of uncertified points (smem)
-// Large K (KP > 128, up to 512): the candidate masks grow to KP/32 words per queued point, so the
-// queue shrinks; the per-cluster Δ (K·M + K int64, 106 KB at K = 512) no longer fits shared memory
-// beside the 2·KP-row B operand and goes straight to global memory (native 64-bit atomics into the
-// pass's partial buffer, fire-and-forget).
+// queue capacity (candidate masks grow with KP: KP/32 words per queued point)
 template <int KP>
 __host__ __device__ constexpr int tc_qcap() { return KP <= 128 ? kQueueCap : 128; }
-template <int KP>
-__host__ __device__ constexpr bool tc_gacc() { return KP > 128; }
-// 64-bit accumulate into the Δ accumulator: shared memory (two 32-bit atomics with carry) or, for
-// the large-K pass, global memory (one native atomic)
-__device__ __forceinline__ void acc_add64(unsigned long long* p, unsigned long long v) {
-  if (__isShared(p)) smem_add64(p, v); else atomicAdd(p, v);
-}
+// 64-bit add into the shared-memory Δ accumulator (two 32-bit atomics with carry)
+__device__ __forceinline__ void acc_add64(unsigned long long* p, unsigned long long v) { smem_add64(p, v); }
 constexpr long long kQueueFlag = 1ll << 62;
 // a queue entry of a point whose label CHANGED (not a recheck): flag | change | row << 16 |
 // (old + 1) << 8 | new.  The recheck warp applies its exact Δ off the epilogue's critical path.
@@ -119,11 +111,11 @@ struct TcBudget {
 #define KM_TS_ABUF 4
 #endif
   // A buffers: per transform group (a group owns buffers g mod a); in TMEM they are cheap
-  static constexpr int a = (tc_a_in_tmem<KP, TR>() ? KM_TS_ABUF : KP > 128 ? 1 : 2) * kTransformGroups;
+  static constexpr int a = (tc_a_in_tmem<KP, TR>() ? KM_TS_ABUF : 2) * kTransformGroups;
   static constexpr int mw = (KP + 31) / 32;
   static constexpr int raw_stride_max = ((TR * MP * 4 + 256 + 1023) / 1024) * 1024;
   static constexpr int fixed = (tc_a_in_tmem<KP, TR>() ? 0 : a * TR * 128) + 2 * KP * 128 +  // A ring, B tile
-                               (tc_gacc<KP>() ? 0 : ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024) +  // Δ accumulators
+                               ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024 +       // Δ accumulators
                                tc_qcap<KP>() * (8 + 4 * mw) + 1024 +                   // recheck queue
                                2048 + 1024 + 8192 +                                    // barriers, align, static
                                tc_pdelta_bytes<MP, KP>();                              // per-warp private Δ
@@ -469,7 +461,7 @@ struct TcSmem {
     off_w = 1024;                             // [2KP rows × 128 B] B operand (SW128)
     off_a = off_w + 2 * KP * 128;             // [AS][TR rows × 128 B]
     off_acc = off_a + (tc_a_in_tmem<KP, TcStages<MP, KP>::TR>() ? 0 : AS * TcStages<MP, KP>::TR * 128);                    // [KP·(MP+1) + KP] int64 Δ
-    off_pacc = off_acc + (tc_gacc<KP>() ? 0 : ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024);  // [kEpiWarps][stride] private Δ
+    off_pacc = off_acc + ((KP * (MP + 1) + KP) * 8 + 1023) / 1024 * 1024;  // [kEpiWarps][stride] private Δ
     off_q = off_pacc + tc_pdelta_bytes<MP, KP>();                            // recheck queue: rows, masks, scalars
     off_raw = off_q + ((tc_qcap<KP>() * (8 + 4 * ((KP + 31) / 32)) + 1024) + 1023) / 1024 * 1024;
     // + 256 B slack: the transform reads MP ≥ m floats per row without bounds branches
@@ -724,9 +716,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   unsigned char* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   float* raw = reinterpret_cast<float*>(sm + S.off_raw);
   unsigned char* s_w = sm + S.off_w;
-  constexpr bool GACC = tc_gacc<KP>();
-  unsigned long long* s_acc = GACC ? a.part : reinterpret_cast<unsigned long long*>(sm + S.off_acc);
-  constexpr bool PD = tc_pdelta<MP, KP>() && !GACC;
+  unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(sm + S.off_acc);
+  constexpr bool PD = tc_pdelta<MP, KP>();
   constexpr int PST = tc_pdelta_stride<MP, KP>();
   unsigned long long* s_pacc = reinterpret_cast<unsigned long long*>(sm + S.off_pacc);
   constexpr int MW = (KP + 31) / 32;                                          // candidate mask words
@@ -785,8 +776,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (!TS)
       for (int i = tid; i < AS * TR * 8; i += nthr)
       *reinterpret_cast<uint4*>(sm + S.off_a + i * 16) = make_uint4(0, 0, 0, 0);
-    if (!GACC)
-      for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
+    for (int i = tid; i < nacc; i += nthr) s_acc[i] = 0ull;
     if (PD)
       for (int i = tid; i < kEpiWarps * PST; i += nthr) s_pacc[i] = 0ull;
     for (int i = tid; i < QCAP; i += nthr) s_q[i] = 0;
@@ -1381,7 +1371,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       if (pst && it < 256) atomicMax(pst + it * 8 + 2, globaltimer());
     }
     if (!resident) {
-      for (int i = tid; i < nacc && !GACC; i += kThreadsTC) {  // one flush of the CTA's Δ
+      for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
         const unsigned long long v = s_acc[i];
         if (v) atomicAdd(a.part + i, v);
       }

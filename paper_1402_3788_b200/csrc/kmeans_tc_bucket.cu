@@ -17,8 +17,6 @@ static int by_kp(const TcArgs& a, int kp, int num_sms, size_t smem_optin, cudaSt
     case 64: return launch_t<MT, 64, true>(a, num_sms, smem_optin, stream, ce, msg, len);
     case 96: return launch_t<MT, 96, true>(a, num_sms, smem_optin, stream, ce, msg, len);
     case 128: return launch_t<MT, 128, true>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 256: return launch_t<MT, 256, true>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 512: return launch_t<MT, 512, true>(a, num_sms, smem_optin, stream, ce, msg, len);
     default: snprintf(msg, len, "tensor-core pass: unsupported k padding %d", kp); return 2;
   }
 }

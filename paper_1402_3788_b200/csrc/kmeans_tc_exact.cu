@@ -13,7 +13,6 @@ static int by_kp(const TcArgs& a, int kp, int num_sms, size_t smem_optin, cudaSt
   switch (kp) {
     case 16: return launch_t<MT, 16, PRE>(a, num_sms, smem_optin, stream, ce, msg, len);
     case 64: return launch_t<MT, 64, PRE>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 512: return launch_t<MT, 512, PRE>(a, num_sms, smem_optin, stream, ce, msg, len);  // cfg4 (K = 512)
     default: return -1;
   }
 }

@@ -126,20 +126,3 @@ def test_tc_large_offset_cancellation(native):
     got = fit(native, x, c0, 8)
     assert got["path"] == 2
     check_vs_oracle(want, got, "offset 1e3")
-
-
-@pytest.mark.parametrize("n,m,k,iters", [(120_000, 25, 512, 4), (80_000, 25, 300, 5), (60_000, 7, 200, 6),
-                                         (50_001, 31, 129, 4)])
-def test_tc_large_k_vs_oracle(native, n, m, k, iters):
-    """The large-K tensor-core pass (KP 256 / 512: N-split MMAs, Δ straight to global memory,
-    16-word candidate masks), forced with path 2, against the oracle; k not a multiple of the
-    padding so padded centres exist; n odd leaves a ragged last tile."""
-    from oracle import oracle
-    from paper_1402_3788_b200.datasets import generate_synthetic_array
-
-    x = generate_synthetic_array(n, m, 64, seed=k + m, dtype=np.float32)
-    c0 = x[:k].astype(np.float64)
-    want = oracle.lloyd(x.astype(np.float64), c0, max_iters=iters, n_workers=8)
-    got = fit(native, x, c0, iters)
-    assert got["path"] == 2
-    check_vs_oracle(want, got, f"large-K {n}x{m}x{k}")
