@@ -42,6 +42,8 @@ struct km_engine {
   // grow-only device buffers (a reload / a new k reuses them when large enough; freed at destroy)
   void* xbuf = nullptr;             // owned points (fp32, or fp64 when narrowing would lose bits)
   void* stage = nullptr;            // fp64 upload staging
+  void* x32 = nullptr;              // fp64 points: fp32 shadow streamed by the tensor-core pass (else null)
+  bool no_shadow = false;           // KM_NO_FP32_SHADOW=1: fp64 points take the SIMT fp64 pass (A/B)
   size_t xbuf_cap = 0, stage_cap = 0, labels_cap = 0, rr_cap = 0, d2_cap = 0, l64_cap = 0, partials_cap = 0;
   // seeding: per-block pair-scan bests, min_d2 argmax partials
   PairBest* pair_best = nullptr;
@@ -286,7 +288,7 @@ static int launch_blocked_mp(km_engine* e, const PassArgs& a, size_t smem, int m
 // tensor-core path: fp32 resident points, m ≤ 31 ([xh|xl] + the ones column fit one 128-byte
 // fp16 row), k ≤ 128 (N = 2·KP ≤ 256 per MMA; 2 warpgroups × 2·KP TMEM columns ≤ 512)
 static bool tc_eligible(const km_engine* e) {
-  return e->point_bytes == 4 && e->m <= 31 && e->kp >= 16 && e->kp <= 128;
+  return (e->point_bytes == 4 || e->x32 != nullptr) && e->m <= 31 && e->kp >= 16 && e->kp <= 128;
 }
 static bool use_tc(const km_engine* e) { return e->path_pref != 1 && e->path_pref != 3 && tc_eligible(e); }
 
@@ -315,7 +317,9 @@ constexpr int KM_RESIDENT_UNFIT = -3;
 static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, bool resident = false,
                      bool no_sums = false, bool skip_first = false) {
   tc::TcArgs a{};
-  a.x = (const float*)e->x;
+  // fp64 points: the pass streams the fp32 shadow; the exact rows come from x64
+  a.x = (const float*)(e->point_bytes == 8 ? e->x32 : e->x);
+  a.x64 = e->point_bytes == 8 ? (const double*)e->x : nullptr;
   a.n = e->n;
   a.m = e->m;
   a.k = e->k;
@@ -331,7 +335,8 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
   a.use_dscale = (F > 120 || F < -120) ? 1 : 0;
   a.scale_f = a.use_dscale ? 1.0f : (float)std::ldexp(1.0, F);
   const int mp = tc_mp_for(e->m);
-  a.err_coef = host_err_coef_tc(e->m, mp);
+  // (+ the fp32 rounding of the shadow coordinates, |fl32(x) − x| ≤ 2⁻²⁴|x|, for fp64 points)
+  a.err_coef = host_err_coef_tc(e->m, mp) + (e->point_bytes == 8 ? (float)std::ldexp(1.0, -22) : 0.f);
   // absolute floor (operand units): fp16 subnormal spacing 2^-24 per element times |w| ≤ 2·max‖x‖·pre
   a.err_floor = (float)((e->m + 2) * std::ldexp(1.0, -23) * (1.0 + 2.0 * e->xnorm_max * e->pre));
   a.nx_inflate = (float)(1.0 + (e->m + 2) * std::ldexp(1.0, -24));
@@ -538,7 +543,8 @@ static FinishArgs finish_args(km_engine* e, int mode, bool accumulate) {
   f.accumulate = accumulate ? 1 : 0;
   f.recheck_count = e->recheck_count;
   f.recheck_rows = nullptr;  // standalone finish: the recheck kernel already re-decided the overflow
-  f.x = (const float*)e->x;
+  f.x = (const float*)(e->point_bytes == 8 ? e->x32 : e->x);
+  f.x64 = e->point_bytes == 8 ? (const double*)e->x : nullptr;
   f.labels = e->labels;
   f.full = 0;
   f.scale_d = std::ldexp(1.0, e->frac_bits);
@@ -762,6 +768,7 @@ static int drop_points(km_engine* e) {
   free_k(e);
   e->seed_ready = false;
   e->x = nullptr;  // an owned copy lives on in xbuf / stage for the next load
+  e->x32 = nullptr;
   e->x_owned = false;
   e->n = 0;
   e->m = 0;
@@ -840,16 +847,17 @@ static int download_labels(km_engine* e, int64_t* out) {
 // ([k·m sums][k counts], zeroed by the caller): one HBM stream, warp-private accumulators where
 // they fit (kmeans_sums.cuh).  Also clears the recheck overflow counter of the pass before it.
 static int launch_sums(km_engine* e, unsigned long long* out) {
-  if (e->point_bytes != 4 || e->m > 31) return set_err(e, KM_ERR_INTERNAL, "cluster-sums kernel: fp32, m <= 31 only");
+  if (e->m > 31) return set_err(e, KM_ERR_INTERNAL, "cluster-sums kernel: m <= 31 only");
+  const bool f64 = e->point_bytes == 8;  // fp64 points: sums of the exact fp64 coordinates
   const size_t per = (size_t)e->k * (e->m + 1) * 8;
   const bool use_d = e->frac_bits > 120 || e->frac_bits < -120;
   // k ≤ 128: cluster-owner warps with register accumulators (no accumulator smem); larger k: the
   // shared-memory accumulator kernel (warp-private where they fit)
   // (the cluster-owner kernel measured 120 µs vs 70 µs for the accumulator kernel at cfg3 — latency-
   // bound ballot loops — so it is only selected with KM_SUMS_OWNER=1)
-  const int kc = !e->sums_owner ? 0 : e->k <= 16 ? 1 : e->k <= 32 ? 2 : e->k <= 64 ? 4 : e->k <= 128 ? 8 : 0;
+  const int kc = !e->sums_owner || f64 ? 0 : e->k <= 16 ? 1 : e->k <= 32 ? 2 : e->k <= 64 ? 4 : e->k <= 128 ? 8 : 0;
   const bool priv = kc == 0 && per * kSumsWarps <= 100 * 1024;
-  const size_t smem = kc ? sums_smem_bytes(e->m, 0, false) : sums_smem_bytes(e->m, e->k, priv);
+  const size_t smem = kc ? sums_smem_bytes(e->m, 0, false) : sums_smem_bytes(e->m, e->k, priv, f64 ? 8 : 4);
   if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
   using Kern = void (*)(const float*, const int32_t*, int64_t, int, int, float, double, unsigned long long*);
   // compile-time feature counts for the BASELINE shapes
@@ -864,28 +872,42 @@ static int launch_sums(km_engine* e, unsigned long long* out) {
   };
   auto accum = [&](auto mt) -> Kern {
     constexpr int MT = decltype(mt)::value;
-    return priv ? (use_d ? cluster_sums_f32_kernel<MT, true, true> : cluster_sums_f32_kernel<MT, true, false>)
-                : (use_d ? cluster_sums_f32_kernel<MT, false, true> : cluster_sums_f32_kernel<MT, false, false>);
+    return priv ? (use_d ? cluster_sums_f32_kernel<float, MT, true, true> : cluster_sums_f32_kernel<float, MT, true, false>)
+                : (use_d ? cluster_sums_f32_kernel<float, MT, false, true> : cluster_sums_f32_kernel<float, MT, false, false>);
   };
   auto pick = [&](auto mt) -> Kern { return kc ? owner(mt) : accum(mt); };
-  Kern kern = e->m == 25 ? pick(std::integral_constant<int, 25>{})
-              : e->m == 10 ? pick(std::integral_constant<int, 10>{})
-              : e->m == 5 ? pick(std::integral_constant<int, 5>{})
-                          : pick(std::integral_constant<int, 0>{});
+  using Kern64 = void (*)(const double*, const int32_t*, int64_t, int, int, float, double, unsigned long long*);
+  Kern kern = nullptr;
+  Kern64 kern64 = nullptr;
+  if (f64) {  // (to_fixed<double> always uses the fp64 scale)
+    kern64 = e->m == 25 ? (priv ? cluster_sums_f32_kernel<double, 25, true, true> : cluster_sums_f32_kernel<double, 25, false, true>)
+                        : (priv ? cluster_sums_f32_kernel<double, 0, true, true> : cluster_sums_f32_kernel<double, 0, false, true>);
+  } else {
+    kern = e->m == 25 ? pick(std::integral_constant<int, 25>{})
+           : e->m == 10 ? pick(std::integral_constant<int, 10>{})
+           : e->m == 5 ? pick(std::integral_constant<int, 5>{})
+                       : pick(std::integral_constant<int, 0>{});
+  }
+  const void* kfn = f64 ? (const void*)kern64 : (const void*)kern;
   // launch geometry per (k, m) shape, computed once (no attribute / occupancy queries per call)
-  const size_t key = ((smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0)) * 64 + (size_t)e->m) * 16 + (size_t)kc;
+  const size_t key = (((smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0)) * 64 + (size_t)e->m) * 16 + (size_t)kc) * 2 + (f64 ? 1 : 0);
   if (e->sums_key != key) {
-    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kSumsThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kSumsThreads, smem));
     e->sums_per_sm = std::max(1, per_sm);
     e->sums_key = key;
   }
   const int64_t ntiles = (e->n + kSumsTile - 1) / kSumsTile;
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((int64_t)e->sums_per_sm * e->num_sms, ntiles));
-  kern<<<(unsigned)grid, kSumsThreads, smem, e->stream>>>((const float*)e->x, e->labels, e->n, e->m, e->k,
-                                                          (float)std::ldexp(1.0, e->frac_bits),
-                                                          std::ldexp(1.0, e->frac_bits), out);
+  if (f64)
+    kern64<<<(unsigned)grid, kSumsThreads, smem, e->stream>>>((const double*)e->x, e->labels, e->n, e->m, e->k,
+                                                              (float)std::ldexp(1.0, e->frac_bits),
+                                                              std::ldexp(1.0, e->frac_bits), out);
+  else
+    kern<<<(unsigned)grid, kSumsThreads, smem, e->stream>>>((const float*)e->x, e->labels, e->n, e->m, e->k,
+                                                            (float)std::ldexp(1.0, e->frac_bits),
+                                                            std::ldexp(1.0, e->frac_bits), out);
   CK_LAUNCH("cluster_sums_f32_kernel");
   e->stats.kernel_launches += 1;
   return KM_OK;
@@ -937,6 +959,7 @@ int km_create(int32_t device, km_engine** out) {
   e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
   e->sums_owner = getenv("KM_SUMS_OWNER") != nullptr;
   e->call_trace = getenv("KM_CALL_TRACE") != nullptr;
+  e->no_shadow = getenv("KM_NO_FP32_SHADOW") != nullptr;
   e->dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
   e->times_path = getenv("KM_TC_TIMES");
   e->num_sms = prop.multiProcessorCount;
@@ -1042,6 +1065,17 @@ int km_load_points_f64(km_engine* e, const double* x, int64_t n, int32_t m) {
   } else {
     e->x = d64;
     e->point_bytes = 8;
+    // fp32 shadow (round to nearest) for the tensor-core filter: the pass streams 4 bytes per
+    // coordinate; the exact fp64 rows are read only by the recheck and the Δ of changed points.
+    // Magnitudes outside the fp32 normal range keep the SIMT fp64 pass (no shadow).
+    const double amax = e->absmax;
+    if (!e->no_shadow && amax < std::ldexp(1.0, 60) && (amax == 0.0 || amax > std::ldexp(1.0, -60))) {
+      if ((r = grow(e, &e->xbuf, &e->xbuf_cap, sizeof(float) * (size_t)count))) return r;
+      narrow_f64_kernel<<<grid_for(e, count, 4), 256, 0, e->stream>>>((const double*)d64, count, (float*)e->xbuf);
+      CK_LAUNCH("narrow_f64_kernel");
+      e->stats.kernel_launches += 1;
+      e->x32 = e->xbuf;
+    }
   }
   e->x_owned = true;
   e->n = n;
@@ -1126,7 +1160,7 @@ int km_update(km_engine* e, int64_t* labels_inout, int32_t k, double* centers_ou
   CK(cudaMemsetAsync(e->part, 0, 8 * ((size_t)k * e->m + k), e->stream));
   // labels were validated on the host: fp32 points with m ≤ 31 take the streaming cluster-sums
   // kernel (kmeans_sums.cuh), other shapes the SIMT pass in sums-only mode
-  if (e->point_bytes == 4 && e->m <= 31) {
+  if (e->m <= 31) {
     if ((r = launch_sums(e, e->part))) return r;
   } else if ((r = launch_pass(e, PASS_SUMS_ONLY, false))) {
     return r;

@@ -12,8 +12,8 @@ namespace km {
 // Exact re-decision of one point by a warp: the reference recurrence (_kernels.py:31-44:
 // features ascending, d = x − c, acc += d·d, no FMA) per centre, lane = centre, argmin with the
 // lowest index on ties.  x_lane holds feature `lane` (m ≤ 32).  Returns the label (all lanes).
-template <int MMAX = 32>
-__device__ __forceinline__ int exact_label_warp(float x_lane, int m, int k, const double* __restrict__ c64) {
+template <int MMAX = 32, typename T = float>
+__device__ __forceinline__ int exact_label_warp(T x_lane, int m, int k, const double* __restrict__ c64) {
   const int lane = threadIdx.x & 31;
   double bd = 0.0;
   int bl = -1;
@@ -96,6 +96,7 @@ struct FinishArgs {
   unsigned int* recheck_count;  // global recheck queue length of the last pass (reset here)
   const long long* recheck_rows;  // global recheck queue (uncertified points not yet re-decided)
   const float* x;            // fp32 points (overflow recheck)
+  const double* x64;         // fp64 points: the exact rows (x is then their fp32 shadow); else null
   int32_t* labels;
   int32_t full;              // the pass had no valid previous labels
   float scale_f;
@@ -214,7 +215,8 @@ __device__ __forceinline__ void recheck_global_queue(FinishArgs& a) {
   const int lane = threadIdx.x & 31, m = a.m, k = a.k;
   for (unsigned int q = threadIdx.x >> 5; q < cnt; q += blockDim.x >> 5) {
     const long long row = a.recheck_rows[q];
-    const float xl = lane < m ? a.x[row * m + lane] : 0.f;
+    // (fp64 points: the exact fp64 row, not the fp32 shadow the pass streamed)
+    const double xl = lane >= m ? 0.0 : a.x64 ? a.x64[row * m + lane] : (double)a.x[row * m + lane];
     const int bl = exact_label_warp(xl, m, k, a.cur);
     const int old = a.full ? -1 : a.labels[row];
     if (bl != old) {
@@ -225,8 +227,8 @@ __device__ __forceinline__ void recheck_global_queue(FinishArgs& a) {
         if (!a.full) atomicAdd(&a.st->changed, 1ull);
       }
       if (lane < m) {
-        const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xl, a.scale_d))
-                                         : __float2ll_rn(__fmul_rn(xl, a.scale_f));
+        const long long v = a.use_dscale || a.x64 ? __double2ll_rn(__dmul_rn(xl, a.scale_d))
+                                                  : __float2ll_rn(__fmul_rn((float)xl, a.scale_f));
         atomicAdd(a.part + (size_t)bl * m + lane, (unsigned long long)v);
         if (old >= 0) atomicAdd(a.part + (size_t)old * m + lane, (unsigned long long)(-v));
       }

@@ -33,16 +33,16 @@ constexpr int kSumsTile = 128;                      // rows per bulk tile (kSums
 constexpr int kSumsStages = 4;                      // tiles in flight per CTA
 
 // shared memory: [stages] × (row tile + labels) ring, then the accumulators
-__host__ __device__ inline size_t sums_stage_bytes(int m) {
-  return (((size_t)kSumsTile * m * 4 + 15) & ~(size_t)15) + kSumsTile * 4;
+__host__ __device__ inline size_t sums_stage_bytes(int m, int esz = 4) {
+  return (((size_t)kSumsTile * m * esz + 15) & ~(size_t)15) + kSumsTile * 4;
 }
-__host__ __device__ inline size_t sums_smem_bytes(int m, int k, bool priv) {
-  return 1024 + kSumsStages * sums_stage_bytes(m) + (size_t)(priv ? kSumsWarps : 1) * k * (m + 1) * 8;
+__host__ __device__ inline size_t sums_smem_bytes(int m, int k, bool priv, int esz = 4) {
+  return 1024 + kSumsStages * sums_stage_bytes(m, esz) + (size_t)(priv ? kSumsWarps : 1) * k * (m + 1) * 8;
 }
 
 // One tile's rows of this warp into its accumulator (lane f ≤ m; lane m counts).
-template <bool PRIV, bool USE_D>
-__device__ __forceinline__ void sums_rows(const float* __restrict__ sx, const int32_t* __restrict__ sl, int r0, int r1,
+template <typename T, bool PRIV, bool USE_D>
+__device__ __forceinline__ void sums_rows(const T* __restrict__ sx, const int32_t* __restrict__ sl, int r0, int r1,
                                           int m, int lane, unsigned long long* acc, int row_len, float scale_f,
                                           double scale_d) {
 #pragma unroll 4
@@ -50,8 +50,7 @@ __device__ __forceinline__ void sums_rows(const float* __restrict__ sx, const in
     const int L = sl[r];                                      // warp-uniform (broadcast)
     unsigned long long q = 1ull;                              // lane m: the count
     if (lane < m) {
-      const float v = sx[r * m + lane];
-      q = (unsigned long long)(USE_D ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f)));
+      q = (unsigned long long)to_fixed<T>(sx[r * m + lane], scale_f, scale_d, USE_D);
     }
     unsigned long long* dst = acc + L * row_len + lane;
     if (PRIV) *dst += q; else smem_add64(dst, q);
@@ -61,30 +60,33 @@ __device__ __forceinline__ void sums_rows(const float* __restrict__ sx, const in
 // Full 128-row tile, compile-time m (MT): the warp's RPW rows at immediate offsets.  The count
 // lane (lane MT) converts cnt_v = 2^-F, which the fixed-point conversion maps to exactly 1, so
 // every lane runs the same instruction stream: ~10 warp instructions per row.
-template <int MT, int RPW, bool PRIV>
-__device__ __forceinline__ void sums_rows_full(const float* __restrict__ sxw, const int32_t* __restrict__ slw,
-                                               int lane, unsigned long long* acc_lane, float scale_f, float cnt_v) {
+template <typename T, int MT, int RPW, bool PRIV>
+__device__ __forceinline__ void sums_rows_full(const T* __restrict__ sxw, const int32_t* __restrict__ slw,
+                                               int lane, unsigned long long* acc_lane, float scale_f, double scale_d,
+                                               T cnt_v) {
   const bool feat = lane < MT;
 #pragma unroll
   for (int j = 0; j < RPW; ++j) {
     const int L = slw[j];
-    const float v = feat ? sxw[j * MT] : cnt_v;
-    const unsigned long long q = (unsigned long long)__float2ll_rn(__fmul_rn(v, scale_f));
+    const T v = feat ? sxw[j * MT] : cnt_v;
+    const unsigned long long q = (unsigned long long)to_fixed<T>(v, scale_f, scale_d, 0);
     unsigned long long* dst = acc_lane + L * (MT + 1);
     if (PRIV) *dst += q; else smem_add64(dst, q);
   }
 }
 
 // MT > 0: compile-time feature count (the full-tile fast path); MT = 0: runtime m
-template <int MT, bool PRIV, bool USE_D>
+// T = float, or double for fp64 points (the fp64 coordinates are what every Δ of those points uses)
+template <typename T, int MT, bool PRIV, bool USE_D>
 __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
-    const float* __restrict__ x, const int32_t* __restrict__ labels, int64_t n, int m, int k, float scale_f,
+    const T* __restrict__ x, const int32_t* __restrict__ labels, int64_t n, int m, int k, float scale_f,
     double scale_d, unsigned long long* __restrict__ out /* [k·m sums][k counts] */) {
   extern __shared__ __align__(1024) unsigned char s_raw[];
   uint64_t* full = reinterpret_cast<uint64_t*>(s_raw);      // [stages]
   uint64_t* empty = full + kSumsStages;                      // [stages]
   unsigned char* ring = s_raw + 1024;
-  const size_t stage = sums_stage_bytes(m);
+  constexpr uint32_t ESZ = sizeof(T);
+  const size_t stage = sums_stage_bytes(m, ESZ);
   const size_t xbytes_max = stage - kSumsTile * 4;
   unsigned long long* s_acc = reinterpret_cast<unsigned long long*>(ring + kSumsStages * stage);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -110,7 +112,7 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
     if (i >= kSumsStages) tc::mbar_wait(empty + s, ((i / kSumsStages) - 1) & 1);
     const int64_t row0 = (t_lo + i) * kSumsTile;
     const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
-    const uint32_t xb = ((uint32_t)rows * m * 4u) & ~15u, lb = ((uint32_t)rows * 4u) & ~15u;
+    const uint32_t xb = ((uint32_t)rows * m * ESZ) & ~15u, lb = ((uint32_t)rows * 4u) & ~15u;
     tc::mbar_arrive_expect_tx(full + s, xb + lb);
     unsigned char* dst = ring + s * stage;
     const uint64_t pol = tc::l2_policy_evict_first();
@@ -118,7 +120,8 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
     if (lb) tc::bulk_g2s_hint(dst + xbytes_max, labels + row0, lb, full + s, pol);
   };
   constexpr int RPW = kSumsTile / kSumsWarps;  // rows per warp and tile
-  const float cnt_v = 1.0f / scale_f;          // = 2^-F: converts to exactly 1 (the count lane)
+  // 2^-F: converts to exactly 1 (the count lane)
+  const T cnt_v = sizeof(T) == 8 ? (T)(1.0 / scale_d) : (T)(1.0f / scale_f);
   if (warp == kSumsWarps) {  // producer warp: one thread keeps the ring full
     if (lane == 0)
       for (int i = 0; i < my; ++i) issue(i);
@@ -131,21 +134,21 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
       // one warp polls the barrier, the others park in bar.sync (no wake-up storms)
       if (warp == 0) tc::mbar_wait(full + s, (i / kSumsStages) & 1);
       tc::named_bar_sync(1, kSumsWarps * 32);
-      float* sx = reinterpret_cast<float*>(ring + s * stage);
+      T* sx = reinterpret_cast<T*>(ring + s * stage);
       int32_t* sl = reinterpret_cast<int32_t*>(ring + s * stage + xbytes_max);
       if (rows < kSumsTile) {  // ragged last tile: patch the sub-granule tail from global memory
-        const uint32_t xe = (((uint32_t)rows * m * 4u) & ~15u) / 4u, le = (((uint32_t)rows * 4u) & ~15u) / 4u;
+        const uint32_t xe = (((uint32_t)rows * m * ESZ) & ~15u) / ESZ, le = (((uint32_t)rows * 4u) & ~15u) / 4u;
         for (uint32_t e = xe + threadIdx.x; e < (uint32_t)rows * m; e += kSumsWarps * 32) sx[e] = __ldg(x + row0 * m + e);
         for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsWarps * 32) sl[e] = __ldg(labels + row0 + e);
         tc::named_bar_sync(1, kSumsWarps * 32);
       }
-      if (MT > 0 && !USE_D && rows == kSumsTile) {
+      if (MT > 0 && (sizeof(T) == 8 || !USE_D) && rows == kSumsTile) {
         if (active)
-          sums_rows_full<(MT > 0 ? MT : 1), RPW, PRIV>(sx + warp * RPW * MT + (lane < m ? lane : 0), sl + warp * RPW, lane,
-                                                       acc + lane, scale_f, cnt_v);
+          sums_rows_full<T, (MT > 0 ? MT : 1), RPW, PRIV>(sx + warp * RPW * MT + (lane < m ? lane : 0), sl + warp * RPW, lane,
+                                                       acc + lane, scale_f, scale_d, cnt_v);
       } else {
         const int r0 = min(warp * RPW, rows), r1 = min(r0 + RPW, rows);
-        if (active) sums_rows<PRIV, USE_D>(sx, sl, r0, r1, m, lane, acc, row_len, scale_f, scale_d);
+        if (active) sums_rows<T, PRIV, USE_D>(sx, sl, r0, r1, m, lane, acc, row_len, scale_f, scale_d);
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(empty + s);

@@ -13,7 +13,8 @@ namespace tc {
 // lowest index on ties), then the same Δ update of the fixed-point sums
 // (global atomics).  One warp per queued point, lane = centre (each lane keeps
 // the reference's sequential feature order); centres staged in shared memory.
-__global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ x, int m, int k,
+__global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ x, const double* __restrict__ x64,
+                                                      int m, int k,
                                                       const double* __restrict__ c64, int32_t* labels,
                                                       const long long* rows, const unsigned int* count,
                                                       unsigned long long* part, float scale_f, double scale_d,
@@ -33,15 +34,15 @@ __global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ 
   const unsigned int warps = (gridDim.x * blockDim.x) >> 5;
   for (unsigned int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < cnt; q += warps) {
     const long long row = rows[q];
-    const float* xr = x + row * m;
-    const float xl = lane < m ? __ldg(xr + lane) : 0.f;  // m ≤ 31 on the tensor-core path
+    // m ≤ 31 on the tensor-core path; fp64 points: the exact row (not the fp32 shadow)
+    const double xl = lane >= m ? 0.0 : x64 ? __ldg(x64 + row * m + lane) : (double)__ldg(x + row * m + lane);
     double bd = 0.0;
     int bl = -1;
     for (int c0 = 0; c0 < k; c0 += 32) {
       const int c = c0 + lane;
       double acc = 0.0;
       for (int f = 0; f < m; ++f) {
-        const double xv = (double)__shfl_sync(0xffffffffu, xl, f);
+        const double xv = __shfl_sync(0xffffffffu, xl, f);
         if (c < k) {
           const double d = __dsub_rn(xv, C[(size_t)c * m + f]);
           acc = __dadd_rn(acc, __dmul_rn(d, d));
@@ -68,8 +69,8 @@ __global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ 
         if (!full) atomicAdd(&st->changed, 1ull);
       }
       if (lane < m) {
-        const long long v = use_dscale ? __double2ll_rn(__dmul_rn((double)xl, scale_d))
-                                       : __float2ll_rn(__fmul_rn(xl, scale_f));
+        const long long v = use_dscale || x64 ? __double2ll_rn(__dmul_rn(xl, scale_d))
+                                              : __float2ll_rn(__fmul_rn((float)xl, scale_f));
         atomicAdd(part + (size_t)bl * m + lane, (unsigned long long)v);
         if (old >= 0) atomicAdd(part + (size_t)old * m + lane, (unsigned long long)(-v));
       }
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(256) recheck_kernel(const float* __restrict__ 
 cudaError_t launch_recheck(const TcArgs& a, int num_sms, cudaStream_t stream) {
   const size_t smem = (size_t)a.k * a.m <= 6144 ? (size_t)a.k * a.m * 8 : 0;
   // one resident warp per queued point (≈ 64 warps/SM): the per-point latency is a few L2 loads
-  recheck_kernel<<<num_sms * 8, 256, smem, stream>>>(a.x, a.m, a.k, a.c64, a.labels, a.recheck_rows, a.recheck_count,
+  recheck_kernel<<<num_sms * 8, 256, smem, stream>>>(a.x, a.x64, a.m, a.k, a.c64, a.labels, a.recheck_rows, a.recheck_count,
                                                      a.part, a.scale_f, a.scale_d, a.use_dscale, a.full, a.no_sums, a.st,
                                                      a.gate);
   return cudaGetLastError();

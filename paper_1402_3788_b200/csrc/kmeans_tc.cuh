@@ -538,14 +538,14 @@ __device__ __forceinline__ void cta_prep_operand(const double* __restrict__ C, i
 // the reference recurrence (features ascending, no FMA) per centre, centres ascending,
 // strict '<' (lowest index on ties).  Non-candidates are strictly farther than the best
 // candidate (filter bound), so the result equals the reference's argmin over all k.
-template <int MP, int MW>
-__device__ __forceinline__ int exact_candidates(const float* __restrict__ gx, int m, const double* __restrict__ C,
-                                                const uint32_t (&mk)[MW], float (&xr)[MP],
+template <int MP, int MW, typename T>
+__device__ __forceinline__ int exact_candidates(const T* __restrict__ gx, int m, const double* __restrict__ C,
+                                                const uint32_t (&mk)[MW], T (&xr)[MP],
                                                 long long* ts = nullptr) {
 #pragma unroll
-  for (int f = 0; f < MP; ++f) xr[f] = (f < m) ? __ldg(gx + f) : 0.f;
+  for (int f = 0; f < MP; ++f) xr[f] = (f < m) ? __ldg(gx + f) : (T)0;
   if (ts) {
-    float sx = 0.f;
+    T sx = 0;
 #pragma unroll
     for (int f = 0; f < MP; ++f) sx += xr[f];
     ts[0] = clock64() + (sx == 12345.f);
@@ -597,28 +597,31 @@ __device__ __forceinline__ int exact_candidates(const float* __restrict__ gx, in
 //    adds it to the new cluster / subtracts it from the old one; lane m moves the counts;
 //  * the first pass (every point adds its row): thread per point, loads batched ahead of the
 //    atomics.
-static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int m, int64_t wrow0, int lane, int bi, int old,
+static __device__ __noinline__ void delta_rows(const float* __restrict__ x, const double* __restrict__ x64, int m,
+                                        int64_t wrow0, int lane, int bi, int old,
                                         unsigned int pend, bool full, unsigned long long* s_acc, int km,
                                         float scale_f, double scale_d, bool use_dscale, bool priv) {
+  // fixed-point value of coordinate f of row r: from the exact fp64 row for fp64 points (x64)
+  auto ldq = [&](int64_t r, int f) -> long long {
+    if (x64) return __double2ll_rn(__dmul_rn(__ldg(x64 + r * m + f), scale_d));
+    const float v = __ldg(x + r * m + f);
+    return use_dscale ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f));
+  };
   // priv: s_acc is this warp's private accumulator — the lane-per-feature path adds without atomics
   auto add = [&](unsigned long long* p, unsigned long long v) {
     if (priv) *p += v; else acc_add64(p, v);
   };
-  auto fixed = [&](float xv) -> long long {
-    return use_dscale ? __double2ll_rn(__dmul_rn((double)xv, scale_d)) : __float2ll_rn(__fmul_rn(xv, scale_f));
-  };
   if (full) {
     if (!((pend >> lane) & 1u)) return;
-    const float* xr = x + (wrow0 + lane) * m;
     constexpr int CH = 8;
     for (int f0 = 0; f0 < m; f0 += CH) {
-      float xv[CH];
+      long long qv[CH];
 #pragma unroll
-      for (int j = 0; j < CH; ++j) xv[j] = (f0 + j < m) ? __ldg(xr + f0 + j) : 0.f;
+      for (int j = 0; j < CH; ++j) qv[j] = (f0 + j < m) ? ldq(wrow0 + lane, f0 + j) : 0ll;
 #pragma unroll
       for (int j = 0; j < CH; ++j) {
         if (f0 + j < m) {
-          const long long v = fixed(xv[j]);
+          const long long v = qv[j];
           acc_add64(s_acc + (size_t)bi * m + f0 + j, (unsigned long long)v);
           if (old >= 0) acc_add64(s_acc + (size_t)old * m + f0 + j, (unsigned long long)(-v));
         }
@@ -635,15 +638,15 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, int 
       src[j] = pend ? __ffs(pend) - 1 : -1;
       if (pend) pend &= pend - 1;
     }
-    float xv[4];
+    long long qv[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) xv[j] = (src[j] >= 0 && lane < m) ? __ldg(x + (wrow0 + src[j]) * m + lane) : 0.f;
+    for (int j = 0; j < 4; ++j) qv[j] = (src[j] >= 0 && lane < m) ? ldq(wrow0 + src[j], lane) : 0ll;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       if (src[j] < 0) break;
       const int nb = __shfl_sync(0xffffffffu, bi, src[j]), ob = __shfl_sync(0xffffffffu, old, src[j]);
       if (lane < m) {
-        const long long v = fixed(xv[j]);
+        const long long v = qv[j];
         add(s_acc + (size_t)nb * m + lane, (unsigned long long)v);
         if (ob >= 0) add(s_acc + (size_t)ob * m + lane, (unsigned long long)(-v));
       } else if (lane == m) {
@@ -813,7 +816,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   __shared__ int s_heavy;
   __shared__ unsigned int s_pass_changes;
   if (tid == 0) {
-    s_heavy = KM_HEAVY_PASSES && !no_sums && (a.full || (resident && a.skip_first)) ? 1 : 0;
+    // (fp64 points: the raw tiles hold the fp32 shadow, not the exact rows — no heavy passes)
+    s_heavy = KM_HEAVY_PASSES && !no_sums && !a.x64 && (a.full || (resident && a.skip_first)) ? 1 : 0;
     s_pass_changes = 0u;
   }
   __syncthreads();
@@ -844,12 +848,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const float* xr = a.x + row * m;
       float xq[MP];
 #pragma unroll
-      for (int f = 0; f < MP; ++f) xq[f] = (f < m) ? __ldg(xr + f) : 0.f;
+      for (int f = 0; f < MP; ++f) xq[f] = (f < m && !a.x64) ? __ldg(xr + f) : 0.f;
 #pragma unroll
       for (int f = 0; f < MP; ++f) {
         if (f < m) {
-          const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
-                                           : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
+          const long long v = a.x64 ? __double2ll_rn(__dmul_rn(__ldg(a.x64 + row * m + f), a.scale_d))
+                              : a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
+                                             : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
           acc_add64(s_acc + (size_t)nw * m + f, (unsigned long long)v);
           if (old >= 0) acc_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
         }
@@ -865,9 +870,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       uint32_t mk[MW];
 #pragma unroll
       for (int w = 0; w < MW; ++w) mk[w] = s_qm[q * MW + w];
-      float xq[MP];
-      const int bl = resident ? exact_candidates<MP, MW>(a.x + row * m, m, s_cbuf + cb * km, mk, xq)
-                              : exact_candidates<MP, MW>(a.x + row * m, m, a.c64, mk, xq);
+      // exact label and fixed-point row (fp64 points: from the exact fp64 coordinates)
+      long long qv[MP];
+      int bl;
+      if (a.x64) {
+        double xq[MP];
+        bl = resident ? exact_candidates<MP, MW>(a.x64 + row * m, m, s_cbuf + cb * km, mk, xq)
+                      : exact_candidates<MP, MW>(a.x64 + row * m, m, a.c64, mk, xq);
+#pragma unroll
+        for (int f = 0; f < MP; ++f) qv[f] = __double2ll_rn(__dmul_rn(xq[f], a.scale_d));
+      } else {
+        float xq[MP];
+        bl = resident ? exact_candidates<MP, MW>(a.x + row * m, m, s_cbuf + cb * km, mk, xq)
+                      : exact_candidates<MP, MW>(a.x + row * m, m, a.c64, mk, xq);
+#pragma unroll
+        for (int f = 0; f < MP; ++f)
+          qv[f] = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
+                               : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
+      }
       if (bl != old) {
         a.labels[row] = bl;
         if (!full) atomicAdd(&st->changed, 1ull);
@@ -875,8 +895,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
 #pragma unroll
         for (int f = 0; f < MP; ++f) {
           if (f < m) {
-            const long long v = a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
-                                             : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
+            const long long v = qv[f];
             acc_add64(s_acc + (size_t)bl * m + f, (unsigned long long)v);
             if (old >= 0) acc_add64(s_acc + (size_t)old * m + f, (unsigned long long)(-v));
           }
@@ -1260,9 +1279,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
               ++my_rechecked;
               const unsigned int slot = atomicAdd(s_qn, 1u);
               if (slot < QCAP) {
-                const float* gr = a.x + (row0 + pp) * m;  // keep the row in L2 until it is re-decided
-                prefetch_l2_keep(gr);
-                prefetch_l2_keep(gr + m - 1);
+                // keep the row in L2 until it is re-decided
+                if (a.x64) {
+                  prefetch_l2_keep(a.x64 + (row0 + pp) * m);
+                  prefetch_l2_keep(a.x64 + (row0 + pp) * m + m - 1);
+                } else {
+                  prefetch_l2_keep(a.x + (row0 + pp) * m);
+                  prefetch_l2_keep(a.x + (row0 + pp) * m + m - 1);
+                }
 #pragma unroll
                 for (int w = 0; w < MW; ++w) s_qm[slot * MW + w] = mk[w];
                 __threadfence_block();  // masks before the entry that publishes them
@@ -1271,8 +1295,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
                     kQueueFlag | ((row0 + pp) << 8) | (long long)(old + 1);
                 bi = old;  // decided by the recheck warp (or the tail)
               } else {     // staging full (rare): decide here
-                float xq[MP];
-                bi = exact_candidates<MP, MW>(a.x + (row0 + pp) * m, m, C, mk, xq);
+                if (a.x64) {
+                  double xq[MP];
+                  bi = exact_candidates<MP, MW>(a.x64 + (row0 + pp) * m, m, C, mk, xq);
+                } else {
+                  float xq[MP];
+                  bi = exact_candidates<MP, MW>(a.x + (row0 + pp) * m, m, C, mk, xq);
+                }
               }
             }
           }
@@ -1308,7 +1337,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
                               a.x + row0 * m, m, 128 * mb + (p & ~31), lane, bi, old, pend, my_acc, km, scale_f,
                               scale_d, use_dscale, PD);
             else
-              delta_rows(a.x, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, my_acc, km, scale_f, scale_d,
+              delta_rows(a.x, a.x64, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, my_acc, km, scale_f, scale_d,
                          use_dscale, PD);
           }
         }
@@ -1338,7 +1367,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     tc_fence_before();
     __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
     if (tid == 0 && pass_tiles > 0) {  // the next pass is heavy if this one changed > 1/256 of the CTA's points
-      s_heavy = KM_HEAVY_PASSES && !no_sums && s_pass_changes * 256u > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
+      s_heavy = KM_HEAVY_PASSES && !no_sums && !a.x64 && s_pass_changes * 256u > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
       s_pass_changes = 0u;
     }
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());

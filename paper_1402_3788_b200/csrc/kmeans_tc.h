@@ -13,7 +13,8 @@ namespace tc {
 constexpr int kTile = 128;
 
 struct TcArgs {
-  const float* x;          // n × m fp32 row-major
+  const float* x;          // n × m fp32 row-major (fp64 points: their fp32 shadow, streamed by the pass)
+  const double* x64;       // fp64 points: the exact rows (recheck, Δ); null for fp32 points
   int64_t n;
   int32_t m, k;
   const unsigned short* wop;  // [2KP][64] fp16 B operand rows ([wh|wh], [wl|0]) from the prep/finish kernel
