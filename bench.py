@@ -115,6 +115,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout=10.0):
+        """Block until nvidia-smi has printed its first sample (its start-up takes ~0.5 s), so the
+        whole timed region is sampled."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+        self.lines.clear()  # (that sample predates the timed region)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
@@ -349,10 +357,11 @@ def run_ours(args):
     torch.cuda.synchronize()
 
     # repetitions of exactly K steps, long enough to sample clocks
-    eng.reset_stats()
-    eng.set_profiling(True)
     sampler = ClockSampler(local)
     sampler.start()
+    sampler.wait_first()
+    eng.reset_stats()
+    eng.set_profiling(True)
     rep_ms, total_iters = [], 0
     t_region = time.perf_counter()
     reps = 0
@@ -374,7 +383,8 @@ def run_ours(args):
         rep_ms.append(ms / iters)
         total_iters += iters
         reps += 1
-        if reps >= args.max_reps or (time.perf_counter() - t_region) >= args.min_seconds:
+        # at least --min-seconds (clock samples) and 10 repetitions; --max-reps caps fast configs
+        if reps >= args.max_reps or ((time.perf_counter() - t_region) >= args.min_seconds and reps >= 10):
             break
     clocks = sampler.stop()
     eng.set_profiling(False)
@@ -505,7 +515,7 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
                     help="N > 1: weak = n rows per GPU (default), strong = n rows in total (default for cfg5)")
     ap.add_argument("--min-seconds", type=float, default=1.0)
-    ap.add_argument("--max-reps", type=int, default=200)
+    ap.add_argument("--max-reps", type=int, default=2000)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--reference-seconds", type=float, default=60.0)

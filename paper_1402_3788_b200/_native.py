@@ -67,7 +67,7 @@ SIGNATURES = {
     "km_assign": (ctypes.c_int, [P, P, I32, P, P]),
     "km_update": (ctypes.c_int, [P, P, I32, P, P]),
     "km_converged": (ctypes.c_int, [P, P, P, I32, I32, F64, ctypes.POINTER(I32)]),
-    "km_lloyd": (ctypes.c_int, [P, P, I32, I32, F64, P, P, P, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
+    "km_lloyd": (ctypes.c_int, [P, P, I32, I32, F64, P, P, P, P, P]),
     "km_wcss": (ctypes.c_int, [P, P, I32, P, ctypes.POINTER(F64)]),
     "km_center_distances": (ctypes.c_int, [P, P, I32, P]),
     "km_diameter": (ctypes.c_int, [P, I64, ctypes.POINTER(F64), ctypes.POINTER(I64), ctypes.POINTER(I64)]),
@@ -155,6 +155,9 @@ class NativeEngine:
         self.device = device
         self.n = 0
         self.m = 0
+        # (iterations, converged) of km_lloyd, written through a cached address
+        self._res = np.zeros(2, dtype=np.int32)
+        self._res_p = self._res.__array_interface__["data"][0]
 
     # -- plumbing ---------------------------------------------------------
     def _check(self, rc):
@@ -224,16 +227,21 @@ class NativeEngine:
         return bool(out.value)
 
     def lloyd(self, c0: np.ndarray, max_iters: int, tol: float, want_labels: bool = True):
+        # (lean: this call is inside every timed bench step — one output buffer for the centres
+        # and counts, raw addresses instead of ctypes pointer objects)
         c0 = np.ascontiguousarray(c0, dtype=np.float64)
         k = c0.shape[0]
-        centers = np.empty((k, self.m), dtype=np.float64)
-        counts = np.empty(k, dtype=np.int64)
+        km = k * self.m
+        out = np.empty(km + k, dtype=np.float64)
+        po = out.__array_interface__["data"][0]
         labels = np.empty(self.n, dtype=np.int64) if want_labels else None
-        iters, conv = I32(0), I32(0)
-        self._check(self._lib.km_lloyd(self._h, _ptr(c0), k, int(max_iters), float(tol), _ptr(centers),
-                                       _ptr(counts), _ptr(labels) if labels is not None else None,
-                                       ctypes.byref(iters), ctypes.byref(conv)))
-        return centers, counts, labels, int(iters.value), bool(conv.value)
+        rc = self._lib.km_lloyd(self._h, c0.__array_interface__["data"][0], k, int(max_iters), float(tol), po,
+                                po + 8 * km, labels.__array_interface__["data"][0] if labels is not None else None,
+                                self._res_p, self._res_p + 4)
+        if rc != KM_OK:
+            self._check(rc)
+        return (out[:km].reshape(k, self.m), out[km:].view(np.int64), labels, int(self._res[0]),
+                bool(self._res[1]))
 
     def wcss(self, centers: np.ndarray, labels: np.ndarray) -> float:
         centers = np.ascontiguousarray(centers, dtype=np.float64)

@@ -105,7 +105,6 @@ struct km_engine {
   // environment knobs, read once at km_create (tuning / A-B experiments only)
   bool full_first_pass = false;     // KM_FULL_FIRST_PASS=1: fused full first pass (epilogue atomics)
   bool no_resident = false;         // KM_NO_RESIDENT=1: launch-per-iteration loop
-  bool sums_owner = false;          // KM_SUMS_OWNER=1: cluster-owner sums kernel (A/B)
   bool call_trace = false;          // KM_CALL_TRACE=1: per-step device/host times of km_lloyd (stderr)
   int dbg_flags = 0;                // KM_TC_DBG
   const char* times_path = nullptr; // KM_TC_TIMES
@@ -851,31 +850,20 @@ static int launch_sums(km_engine* e, unsigned long long* out) {
   const bool f64 = e->point_bytes == 8;  // fp64 points: sums of the exact fp64 coordinates
   const size_t per = (size_t)e->k * (e->m + 1) * 8;
   const bool use_d = e->frac_bits > 120 || e->frac_bits < -120;
-  // k ≤ 128: cluster-owner warps with register accumulators (no accumulator smem); larger k: the
-  // shared-memory accumulator kernel (warp-private where they fit)
-  // (the cluster-owner kernel measured 120 µs vs 70 µs for the accumulator kernel at cfg3 — latency-
-  // bound ballot loops — so it is only selected with KM_SUMS_OWNER=1)
-  const int kc = !e->sums_owner || f64 ? 0 : e->k <= 16 ? 1 : e->k <= 32 ? 2 : e->k <= 64 ? 4 : e->k <= 128 ? 8 : 0;
-  const bool priv = kc == 0 && per * kSumsWarps <= 100 * 1024;
-  const size_t smem = kc ? sums_smem_bytes(e->m, 0, false) : sums_smem_bytes(e->m, e->k, priv, f64 ? 8 : 4);
+  // shared-memory accumulators, warp-private where they fit.  (Measured and dropped: cluster-owner
+  // warps with register accumulators, 120 µs vs 70 µs at cfg3; label-grouped 32-row batches,
+  // 133 µs — both latency-bound ballot loops.)
+  const bool priv = per * kSumsWarps <= 100 * 1024;
+  const size_t smem = sums_smem_bytes(e->m, e->k, priv, f64 ? 8 : 4);
   if (smem > e->smem_optin) return set_err(e, KM_ERR_CAPACITY, "cluster-sums kernel: k·m too large for shared memory");
   using Kern = void (*)(const float*, const int32_t*, int64_t, int, int, float, double, unsigned long long*);
   // compile-time feature counts for the BASELINE shapes
-  auto owner = [&](auto mt) -> Kern {
-    constexpr int MT = decltype(mt)::value;
-    switch (kc) {
-      case 1: return use_d ? cluster_sums_owner_kernel<MT, 1, true> : cluster_sums_owner_kernel<MT, 1, false>;
-      case 2: return use_d ? cluster_sums_owner_kernel<MT, 2, true> : cluster_sums_owner_kernel<MT, 2, false>;
-      case 4: return use_d ? cluster_sums_owner_kernel<MT, 4, true> : cluster_sums_owner_kernel<MT, 4, false>;
-      default: return use_d ? cluster_sums_owner_kernel<MT, 8, true> : cluster_sums_owner_kernel<MT, 8, false>;
-    }
-  };
   auto accum = [&](auto mt) -> Kern {
     constexpr int MT = decltype(mt)::value;
     return priv ? (use_d ? cluster_sums_f32_kernel<float, MT, true, true> : cluster_sums_f32_kernel<float, MT, true, false>)
                 : (use_d ? cluster_sums_f32_kernel<float, MT, false, true> : cluster_sums_f32_kernel<float, MT, false, false>);
   };
-  auto pick = [&](auto mt) -> Kern { return kc ? owner(mt) : accum(mt); };
+  auto pick = [&](auto mt) -> Kern { return accum(mt); };
   using Kern64 = void (*)(const double*, const int32_t*, int64_t, int, int, float, double, unsigned long long*);
   Kern kern = nullptr;
   Kern64 kern64 = nullptr;
@@ -890,7 +878,7 @@ static int launch_sums(km_engine* e, unsigned long long* out) {
   }
   const void* kfn = f64 ? (const void*)kern64 : (const void*)kern;
   // launch geometry per (k, m) shape, computed once (no attribute / occupancy queries per call)
-  const size_t key = (((smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0)) * 64 + (size_t)e->m) * 16 + (size_t)kc) * 2 + (f64 ? 1 : 0);
+  const size_t key = ((smem * 4 + (priv ? 1 : 0) + (use_d ? 2 : 0)) * 64 + (size_t)e->m) * 2 + (f64 ? 1 : 0);
   if (e->sums_key != key) {
     CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -957,7 +945,6 @@ int km_create(int32_t device, km_engine** out) {
   e->device = device;
   e->full_first_pass = getenv("KM_FULL_FIRST_PASS") && atoi(getenv("KM_FULL_FIRST_PASS")) != 0;
   e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
-  e->sums_owner = getenv("KM_SUMS_OWNER") != nullptr;
   e->call_trace = getenv("KM_CALL_TRACE") != nullptr;
   e->no_shadow = getenv("KM_NO_FP32_SHADOW") != nullptr;
   e->dbg_flags = getenv("KM_TC_DBG") ? atoi(getenv("KM_TC_DBG")) : 0;
@@ -1240,11 +1227,19 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
   };
   trace();
   if (!resume) {
-    std::memcpy(pin_c0, c0, 8 * km);
-    CK(cudaMemcpyAsync(e->cur, pin_c0, 8 * km, cudaMemcpyHostToDevice, e->stream));
+    // C0: in the begin kernel's parameters when it fits, else one pinned H2D copy
+    C0Inline c0p;  // (by-value launch parameter; only the first k·m entries are read)
+    const bool inl = km <= (size_t)kC0Inline;
+    if (inl) {
+      std::memcpy(c0p.v, c0, 8 * km);
+    } else {
+      std::memcpy(pin_c0, c0, 8 * km);
+      CK(cudaMemcpyAsync(e->cur, pin_c0, 8 * km, cudaMemcpyHostToDevice, e->stream));
+    }
     lloyd_begin_kernel<<<1, 512, 0, e->stream>>>(e->st, max_iters, tol, e->part, e->tot, e->dlt, nacc, e->grid_sync,
                                                  e->recheck_count, e->cur, e->w, e->cn, e->cmax, k, m, e->mpad,
-                                                 tc_eligible(e) ? e->wop : nullptr, e->kp, e->pre);
+                                                 tc_eligible(e) ? e->wop : nullptr, e->kp, e->pre, c0p,
+                                                 inl ? (int)km : 0);
     CK_LAUNCH("lloyd_begin_kernel launch");
     e->stats.kernel_launches += 1;
     e->resident_zeroed = true;
@@ -1281,10 +1276,11 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
     if ((r = launch_tc(e, full, true, false, true, false, skip))) return r;
     trace();
     if (e->profiling) CK(cudaEventRecord(ev1, e->stream));
-    // one round trip: state + (if the loop is done) the model
-    CK(cudaMemcpyAsync(hs, e->st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaMemcpyAsync(pin_c, e->cur, 8 * km, cudaMemcpyDeviceToHost, e->stream));
-    CK(cudaMemcpyAsync(pin_n, e->model_counts, 8 * (size_t)k, cudaMemcpyDeviceToHost, e->stream));
+    // one round trip: state + (if the loop is done) the model, written into the pinned staging by
+    // one small kernel (mapped host memory)
+    lloyd_publish_kernel<<<1, 256, 0, e->stream>>>(e->st, e->cur, e->model_counts, (int)km, k, hs, pin_c, pin_n);
+    CK_LAUNCH("lloyd_publish_kernel launch");
+    e->stats.kernel_launches += 1;
     CK(cudaStreamSynchronize(e->stream));
     e->stats.host_syncs += 1;
     if (e->call_trace && nt > 1) {

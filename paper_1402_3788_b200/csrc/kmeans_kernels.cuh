@@ -670,13 +670,25 @@ __global__ void __launch_bounds__(512) prep_filter_kernel(const double* c, float
 // Start of a resident Lloyd run (km_lloyd, tensor-core path), one launch instead of a state
 // upload + five memsets + the prep kernel: loop state {max_iters, tol}, zeroed Δ / totals /
 // rotating delta buffers / grid-barrier counter / recheck counter, and the filter operands of C0.
+// C0 of a km_lloyd call passed by value in the begin kernel's launch parameters when it fits
+// (k·m ≤ 480: no host→device copy in front of the run)
+constexpr int kC0Inline = 480;
+struct C0Inline {
+  double v[kC0Inline];
+};
+
 __global__ void __launch_bounds__(512) lloyd_begin_kernel(DevState* st, int max_iters, double tol,
                                                           unsigned long long* part, unsigned long long* tot,
                                                           unsigned long long* dlt, size_t nacc,
                                                           unsigned int* grid_sync, unsigned int* recheck_count,
-                                                          const double* c, float* w, float* cn, float* cmax, int k,
-                                                          int m, int mpad, unsigned short* wop, int kp, float pre) {
+                                                          double* c, float* w, float* cn, float* cmax, int k,
+                                                          int m, int mpad, unsigned short* wop, int kp, float pre,
+                                                          const __grid_constant__ C0Inline c0, int c0_n) {
   __shared__ float s_red[32];
+  if (c0_n > 0) {  // C0 from the launch parameters (else the caller copied it to c)
+    for (int i = threadIdx.x; i < c0_n; i += blockDim.x) c[i] = c0.v[i];
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     DevState s{};
     s.max_iters = max_iters;
@@ -691,6 +703,16 @@ __global__ void __launch_bounds__(512) lloyd_begin_kernel(DevState* st, int max_
   }
   for (size_t i = threadIdx.x; i < 3 * nacc; i += blockDim.x) dlt[i] = 0ull;
   block_prep_filter(c, w, cn, cmax, k, m, mpad, s_red, wop, kp, pre);
+}
+
+// End of a km_lloyd call: state, centres and counts straight into the caller's pinned (mapped)
+// staging — one launch instead of three device→host copies.
+__global__ void __launch_bounds__(256) lloyd_publish_kernel(const DevState* st, const double* cur,
+                                                            const long long* counts, int km, int k, DevState* h_st,
+                                                            double* h_c, long long* h_n) {
+  if (threadIdx.x == 0) *h_st = *st;
+  for (int i = threadIdx.x; i < km; i += blockDim.x) h_c[i] = cur[i];
+  for (int i = threadIdx.x; i < k; i += blockDim.x) h_n[i] = counts[i];
 }
 
 // Standalone congruence test (km_converged).

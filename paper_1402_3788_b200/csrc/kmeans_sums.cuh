@@ -166,105 +166,4 @@ __global__ void __launch_bounds__(kSumsThreads) cluster_sums_f32_kernel(
   }
 }
 
-// Cluster-owner form (k ≤ 16·KC): warp w owns clusters w, w + 16, … and keeps their sums in
-// REGISTERS (lane f = feature f); per 32-row group of a tile it takes a ballot of the rows whose
-// label it owns and adds just those rows (the count is the ballot's popcount).  Per row: one
-// shared-memory load of the coordinates by the owning warp — no accumulator traffic in shared
-// memory, no atomics (the accumulator version spent ~6 shared-memory wavefronts per row).
-template <int MT, int KC, bool USE_D>
-__global__ void __launch_bounds__(kSumsThreads) cluster_sums_owner_kernel(
-    const float* __restrict__ x, const int32_t* __restrict__ labels, int64_t n, int m, int k, float scale_f,
-    double scale_d, unsigned long long* __restrict__ out /* [k·m sums][k counts] */) {
-  extern __shared__ __align__(1024) unsigned char s_raw[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(s_raw);
-  uint64_t* empty = full + kSumsStages;
-  unsigned char* ring = s_raw + 1024;
-  const size_t stage = sums_stage_bytes(m);
-  const size_t xbytes_max = stage - kSumsTile * 4;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mm = MT > 0 ? MT : m;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kSumsStages; ++s) {
-      tc::mbar_init(full + s, 1);
-      tc::mbar_init(empty + s, kSumsWarps);
-    }
-    tc::fence_barrier_init();
-  }
-  __syncthreads();
-  const int64_t ntiles = (n + kSumsTile - 1) / kSumsTile;
-  const int64_t t_lo = ntiles * blockIdx.x / gridDim.x, t_hi = ntiles * (blockIdx.x + 1) / gridDim.x;
-  const int my = (int)(t_hi - t_lo);
-  if (warp == kSumsWarps) {  // producer warp
-    if (lane == 0) {
-      const uint64_t pol = tc::l2_policy_evict_first();
-      for (int i = 0; i < my; ++i) {
-        const int s = i % kSumsStages;
-        if (i >= kSumsStages) tc::mbar_wait(empty + s, ((i / kSumsStages) - 1) & 1);
-        const int64_t row0 = (t_lo + i) * kSumsTile;
-        const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
-        const uint32_t xb = ((uint32_t)rows * mm * 4u) & ~15u, lb = ((uint32_t)rows * 4u) & ~15u;
-        tc::mbar_arrive_expect_tx(full + s, xb + lb);
-        unsigned char* dst = ring + s * stage;
-        if (xb) tc::bulk_g2s_hint(dst, x + row0 * mm, xb, full + s, pol);
-        if (lb) tc::bulk_g2s_hint(dst + xbytes_max, labels + row0, lb, full + s, pol);
-      }
-    }
-    return;
-  }
-  unsigned long long acc[KC];
-  unsigned int cnt[KC];
-#pragma unroll
-  for (int j = 0; j < KC; ++j) {
-    acc[j] = 0ull;
-    cnt[j] = 0u;
-  }
-  const bool feat = lane < mm;
-  for (int i = 0; i < my; ++i) {
-    const int s = i % kSumsStages;
-    const int64_t row0 = (t_lo + i) * kSumsTile;
-    const int rows = (int)(n - row0 < kSumsTile ? n - row0 : kSumsTile);
-    if (warp == 0) tc::mbar_wait(full + s, (i / kSumsStages) & 1);
-    tc::named_bar_sync(1, kSumsWarps * 32);
-    float* sx = reinterpret_cast<float*>(ring + s * stage);
-    int32_t* sl = reinterpret_cast<int32_t*>(ring + s * stage + xbytes_max);
-    if (rows < kSumsTile) {  // ragged last tile: patch the sub-granule tail from global memory
-      const uint32_t xe = (((uint32_t)rows * mm * 4u) & ~15u) >> 2, le = (((uint32_t)rows * 4u) & ~15u) >> 2;
-      for (uint32_t e = xe + threadIdx.x; e < (uint32_t)rows * mm; e += kSumsWarps * 32) sx[e] = __ldg(x + row0 * mm + e);
-      for (uint32_t e = le + threadIdx.x; e < (uint32_t)rows; e += kSumsWarps * 32) sl[e] = __ldg(labels + row0 + e);
-      tc::named_bar_sync(1, kSumsWarps * 32);
-    }
-#pragma unroll
-    for (int q = 0; q < kSumsTile / 32; ++q) {
-      const int r = q * 32 + lane;
-      const int lab = r < rows ? sl[r] : -1;
-#pragma unroll
-      for (int j = 0; j < KC; ++j) {
-        const int c = warp + kSumsWarps * j;
-        unsigned int mask = __ballot_sync(0xffffffffu, lab == c);
-        cnt[j] += __popc(mask);
-        while (mask) {
-          const int b = __ffs(mask) - 1;
-          mask &= mask - 1;
-          if (feat) {
-            const float v = sx[(q * 32 + b) * mm + lane];
-            acc[j] += (unsigned long long)(USE_D ? __double2ll_rn(__dmul_rn((double)v, scale_d))
-                                                 : __float2ll_rn(__fmul_rn(v, scale_f)));
-          }
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(empty + s);
-  }
-  // one global atomic per (owned cluster, feature) and warp
-#pragma unroll
-  for (int j = 0; j < KC; ++j) {
-    const int c = warp + kSumsWarps * j;
-    if (c < k) {
-      if (feat && acc[j]) atomicAdd(out + (size_t)c * mm + lane, acc[j]);
-      if (lane == 0 && cnt[j]) atomicAdd(out + (size_t)k * mm + c, (unsigned long long)cnt[j]);
-    }
-  }
-}
-
 }  // namespace km

@@ -90,6 +90,7 @@ cudaError_t launch_recheck(const TcArgs& a, int num_sms, cudaStream_t stream) {
 
 int launch(const TcArgs& a, int mp, int kp, int num_sms, size_t smem_optin, cudaStream_t stream,
            cudaError_t* ce, char* msg, size_t len) {
+  if (a.x64) return launch_f64(a, a.m, mp, kp, num_sms, smem_optin, stream, ce, msg, len);
   if (a.exact_m) {
     const int r = launch_exact(a, a.m, kp, a.prescale != 0, num_sms, smem_optin, stream, ce, msg, len);
     if (r >= 0) return r;

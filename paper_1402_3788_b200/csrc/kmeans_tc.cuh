@@ -597,13 +597,14 @@ __device__ __forceinline__ int exact_candidates(const T* __restrict__ gx, int m,
 //    adds it to the new cluster / subtracts it from the old one; lane m moves the counts;
 //  * the first pass (every point adds its row): thread per point, loads batched ahead of the
 //    atomics.
+template <bool X64>
 static __device__ __noinline__ void delta_rows(const float* __restrict__ x, const double* __restrict__ x64, int m,
                                         int64_t wrow0, int lane, int bi, int old,
                                         unsigned int pend, bool full, unsigned long long* s_acc, int km,
                                         float scale_f, double scale_d, bool use_dscale, bool priv) {
   // fixed-point value of coordinate f of row r: from the exact fp64 row for fp64 points (x64)
   auto ldq = [&](int64_t r, int f) -> long long {
-    if (x64) return __double2ll_rn(__dmul_rn(__ldg(x64 + r * m + f), scale_d));
+    if (X64) return __double2ll_rn(__dmul_rn(__ldg(x64 + r * m + f), scale_d));
     const float v = __ldg(x + r * m + f);
     return use_dscale ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f));
   };
@@ -686,9 +687,12 @@ static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__
   }
 }
 
-template <int MT, int KP, bool PRE>
+// X64: fp64 points — the pass streams their fp32 shadow (a.x), the exact rows (a.x64) feed the
+// recheck and the Δ; a separate instantiation so the fp32 kernels carry none of it
+template <int MT, int KP, bool PRE, bool X64>
 __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
   static_assert(kThreadsTC == (kTransformWarps + kEpiWarps + 4) * 32, "warp-role layout");
+  const double* __restrict__ x64p = X64 ? a.x64 : nullptr;
   constexpr int MP = MT > 0 ? MT : -MT;
   if (a.gate && (a.st->done || a.st->need_host)) return;
   using L = TcLayout<MP>;
@@ -817,7 +821,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   __shared__ unsigned int s_pass_changes;
   if (tid == 0) {
     // (fp64 points: the raw tiles hold the fp32 shadow, not the exact rows — no heavy passes)
-    s_heavy = KM_HEAVY_PASSES && !no_sums && !a.x64 && (a.full || (resident && a.skip_first)) ? 1 : 0;
+    s_heavy = KM_HEAVY_PASSES && !no_sums && !x64p && (a.full || (resident && a.skip_first)) ? 1 : 0;
     s_pass_changes = 0u;
   }
   __syncthreads();
@@ -848,11 +852,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       const float* xr = a.x + row * m;
       float xq[MP];
 #pragma unroll
-      for (int f = 0; f < MP; ++f) xq[f] = (f < m && !a.x64) ? __ldg(xr + f) : 0.f;
+      for (int f = 0; f < MP; ++f) xq[f] = (f < m && !x64p) ? __ldg(xr + f) : 0.f;
 #pragma unroll
       for (int f = 0; f < MP; ++f) {
         if (f < m) {
-          const long long v = a.x64 ? __double2ll_rn(__dmul_rn(__ldg(a.x64 + row * m + f), a.scale_d))
+          const long long v = x64p ? __double2ll_rn(__dmul_rn(__ldg(x64p + row * m + f), a.scale_d))
                               : a.use_dscale ? __double2ll_rn(__dmul_rn((double)xq[f], a.scale_d))
                                              : __float2ll_rn(__fmul_rn(xq[f], a.scale_f));
           acc_add64(s_acc + (size_t)nw * m + f, (unsigned long long)v);
@@ -873,10 +877,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       // exact label and fixed-point row (fp64 points: from the exact fp64 coordinates)
       long long qv[MP];
       int bl;
-      if (a.x64) {
+      if (x64p) {
         double xq[MP];
-        bl = resident ? exact_candidates<MP, MW>(a.x64 + row * m, m, s_cbuf + cb * km, mk, xq)
-                      : exact_candidates<MP, MW>(a.x64 + row * m, m, a.c64, mk, xq);
+        bl = resident ? exact_candidates<MP, MW>(x64p + row * m, m, s_cbuf + cb * km, mk, xq)
+                      : exact_candidates<MP, MW>(x64p + row * m, m, a.c64, mk, xq);
 #pragma unroll
         for (int f = 0; f < MP; ++f) qv[f] = __double2ll_rn(__dmul_rn(xq[f], a.scale_d));
       } else {
@@ -1280,9 +1284,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
               const unsigned int slot = atomicAdd(s_qn, 1u);
               if (slot < QCAP) {
                 // keep the row in L2 until it is re-decided
-                if (a.x64) {
-                  prefetch_l2_keep(a.x64 + (row0 + pp) * m);
-                  prefetch_l2_keep(a.x64 + (row0 + pp) * m + m - 1);
+                if (x64p) {
+                  prefetch_l2_keep(x64p + (row0 + pp) * m);
+                  prefetch_l2_keep(x64p + (row0 + pp) * m + m - 1);
                 } else {
                   prefetch_l2_keep(a.x + (row0 + pp) * m);
                   prefetch_l2_keep(a.x + (row0 + pp) * m + m - 1);
@@ -1295,9 +1299,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
                     kQueueFlag | ((row0 + pp) << 8) | (long long)(old + 1);
                 bi = old;  // decided by the recheck warp (or the tail)
               } else {     // staging full (rare): decide here
-                if (a.x64) {
+                if (x64p) {
                   double xq[MP];
-                  bi = exact_candidates<MP, MW>(a.x64 + (row0 + pp) * m, m, C, mk, xq);
+                  bi = exact_candidates<MP, MW>(x64p + (row0 + pp) * m, m, C, mk, xq);
                 } else {
                   float xq[MP];
                   bi = exact_candidates<MP, MW>(a.x + (row0 + pp) * m, m, C, mk, xq);
@@ -1337,7 +1341,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
                               a.x + row0 * m, m, 128 * mb + (p & ~31), lane, bi, old, pend, my_acc, km, scale_f,
                               scale_d, use_dscale, PD);
             else
-              delta_rows(a.x, a.x64, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, my_acc, km, scale_f, scale_d,
+              delta_rows<X64>(a.x, x64p, m, row0 + 128 * mb + (p & ~31), lane, bi, old, pend, full, my_acc, km, scale_f, scale_d,
                          use_dscale, PD);
           }
         }
@@ -1367,7 +1371,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     tc_fence_before();
     __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
     if (tid == 0 && pass_tiles > 0) {  // the next pass is heavy if this one changed > 1/256 of the CTA's points
-      s_heavy = KM_HEAVY_PASSES && !no_sums && !a.x64 && s_pass_changes * 256u > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
+      s_heavy = KM_HEAVY_PASSES && !no_sums && !x64p && s_pass_changes * 256u > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
       s_pass_changes = 0u;
     }
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
@@ -1631,10 +1635,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   }
 }
 
-template <int MT, int KP, bool PRE>
+template <int MT, int KP, bool PRE, bool X64>
 inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_t stream, cudaError_t* ce, char* msg,
                     size_t len) {
-  auto kern = lloyd_pass_tc_kernel<MT, KP, PRE>;
+  auto kern = lloyd_pass_tc_kernel<MT, KP, PRE, X64>;
   constexpr int MP = MT > 0 ? MT : -MT;
   // per-instantiation launch facts, queried once (a launch is otherwise one cudaLaunchKernelEx):
   // static smem, and the largest dynamic smem size already granted to the function

@@ -11,12 +11,12 @@ template <int MT>
 static int by_kp(const TcArgs& a, int kp, int num_sms, size_t smem_optin, cudaStream_t stream, cudaError_t* ce,
                  char* msg, size_t len) {
   switch (kp) {
-    case 16: return launch_t<MT, 16, true>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 32: return launch_t<MT, 32, true>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 48: return launch_t<MT, 48, true>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 64: return launch_t<MT, 64, true>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 96: return launch_t<MT, 96, true>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 128: return launch_t<MT, 128, true>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 16: return launch_t<MT, 16, true, false>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 32: return launch_t<MT, 32, true, false>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 48: return launch_t<MT, 48, true, false>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 64: return launch_t<MT, 64, true, false>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 96: return launch_t<MT, 96, true, false>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 128: return launch_t<MT, 128, true, false>(a, num_sms, smem_optin, stream, ce, msg, len);
     default: snprintf(msg, len, "tensor-core pass: unsupported k padding %d", kp); return 2;
   }
 }

@@ -11,8 +11,8 @@ template <int MT, bool PRE>
 static int by_kp(const TcArgs& a, int kp, int num_sms, size_t smem_optin, cudaStream_t stream, cudaError_t* ce,
                  char* msg, size_t len) {
   switch (kp) {
-    case 16: return launch_t<MT, 16, PRE>(a, num_sms, smem_optin, stream, ce, msg, len);
-    case 64: return launch_t<MT, 64, PRE>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 16: return launch_t<MT, 16, PRE, false>(a, num_sms, smem_optin, stream, ce, msg, len);
+    case 64: return launch_t<MT, 64, PRE, false>(a, num_sms, smem_optin, stream, ce, msg, len);
     default: return -1;
   }
 }
