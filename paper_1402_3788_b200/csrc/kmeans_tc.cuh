@@ -1203,8 +1203,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
           const uint32_t tcol = tmem + lane_base + ss * TM::per + mb * SC;
           // Certification: best = min score, candidates = {c : score ≤ best + E2}; the point is
           // certified iff the best is the only candidate (then it is the reference's argmin).
-          // One packed counter per point: +1 per candidate, + c·2^8 (the index sum = the
-          // argmin when there is one candidate).  KP ≤ 32: the scores stay in registers.
+          // The candidate mask is built with one compare + select per centre (no serial counter
+          // chain); count = popcount, argmin = the lowest set bit.  KP ≤ 32: the scores stay in
+          // registers between the min and the mask.
           constexpr int NCH = KP / 16;
           constexpr bool KEEP = KP <= 32;
           float vk[KEEP ? KP : 16];
@@ -1233,18 +1234,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
             best = fminf(best, fminf(fminf(m4[0], m4[1]), fminf(m4[2], m4[3])));
           }
           const float thr = exact_only ? __int_as_float(0x7f800000) : best + E2;
-          uint32_t cnt = 0;  // candidates | index sum << 8
           uint32_t mk[MW];
 #pragma unroll
           for (int w = 0; w < MW; ++w) mk[w] = 0u;
-          if constexpr (KEEP) {
-            // count and index sum only (FSETP + predicated add per centre); the candidate mask is
-            // built for uncertified points alone (below)
 #pragma unroll
-            for (int c = 0; c < KP; ++c) cnt += vk[c] <= thr ? (1u + ((uint32_t)c << 8)) : 0u;
-          }
-#pragma unroll
-          for (int ch = 0; ch < (KEEP ? 0 : NCH); ++ch) {
+          for (int ch = 0; ch < NCH; ++ch) {
             if (!KEEP) {
               uint32_t r0[16], r1[16];
               tmem_ld16(tcol + ch * 16, r0);
@@ -1254,23 +1248,24 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
               for (int jj = 0; jj < 16; ++jj)
                 vk[jj] = K3 ? __uint_as_float(r0[jj]) : __uint_as_float(r0[jj]) + __uint_as_float(r1[jj]);
             }
-            uint32_t bits = 0;
+            // 16 bits as a sum of disjoint selected powers of two (adds pair up into IADD3 trees)
+            uint32_t b[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-            for (int jj = 0; jj < 16; ++jj) {
-              const bool cand = vk[KEEP ? ch * 16 + jj : jj] <= thr;
-              cnt += cand ? (1u + ((uint32_t)(ch * 16 + jj) << 8)) : 0u;
-              bits |= cand ? (1u << jj) : 0u;
-            }
-            mk[(ch * 16) >> 5] |= bits << ((ch * 16) & 31);
+            for (int jj = 0; jj < 16; ++jj)
+              b[jj & 3] += vk[KEEP ? ch * 16 + jj : jj] <= thr ? (1u << jj) : 0u;
+            mk[(ch * 16) >> 5] += ((b[0] + b[1]) + (b[2] + b[3])) << ((ch * 16) & 31);
           }
-          int bi = (KM_DBG_FLAGS & 512) ? old : (int)(cnt >> 8);  // (dbg 512: timing only, labels frozen)
-          const bool unc = active && (cnt & 0xff) != 1u && !(KM_DBG_FLAGS & (256 | 512));  // (dbg 256: timing only)
+          uint32_t ncand = 0;
+          int first = -1;
+#pragma unroll
+          for (int w = MW - 1; w >= 0; --w) {
+            ncand += __popc(mk[w]);
+            if (mk[w]) first = 32 * w + __ffs(mk[w]) - 1;
+          }
+          int bi = (KM_DBG_FLAGS & 512) ? old : first;  // (dbg 512: timing only, labels frozen)
+          const bool unc = active && ncand != 1u && !(KM_DBG_FLAGS & (256 | 512));  // (dbg 256: timing only)
           if (__any_sync(0xffffffffu, unc)) {
             if (unc) {
-              if constexpr (KEEP) {  // the candidate mask (uncertified points only)
-#pragma unroll
-                for (int c = 0; c < KP; ++c) mk[c >> 5] |= (vk[c] <= thr ? 1u : 0u) << (c & 31);
-              }
               // padded centres (c ≥ k) are never candidates, whatever the threshold (exact_only
               // sets it to +inf): the recheck only ever reads real centre rows
 #pragma unroll

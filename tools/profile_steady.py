@@ -10,7 +10,8 @@ import numpy as np
 from paper_1402_3788_b200 import _native
 from paper_1402_3788_b200.datasets import generate_synthetic_array
 
-CFG = {"cfg1": (10_000, 5, 4), "cfg2": (100_000, 10, 8), "cfg3": (2_000_000, 25, 16), "cfg4": (2_000_000, 25, 512)}
+CFG = {"cfg1": (10_000, 5, 4), "cfg2": (100_000, 10, 8), "cfg3": (2_000_000, 25, 16), "cfg4": (2_000_000, 25, 512),
+       "k64": (2_000_000, 25, 64)}
 name = sys.argv[1] if len(sys.argv) > 1 else "cfg3"
 warm = int(sys.argv[2]) if len(sys.argv) > 2 else 400
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 50
