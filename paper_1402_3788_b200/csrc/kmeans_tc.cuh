@@ -664,25 +664,70 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, cons
 // `prow0`: row in the tile of lane 0's point; rows past the tile's 16-byte bulk come from global.
 static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__ rs, uint32_t bulk_elems,
                                                        const float* __restrict__ gx_tile, int m, int prow0, int lane,
-                                                       int bi, int old, unsigned int pend, unsigned long long* s_acc,
-                                                       int km, float scale_f, double scale_d, bool use_dscale,
-                                                       bool priv) {
-  auto add = [&](unsigned long long* p, unsigned long long v) {
-    if (priv) *p += v; else acc_add64(p, v);
+                                                       int bi, int old, unsigned int pend,
+                                                       unsigned long long* __restrict__ s_acc, int km, float scale_f,
+                                                       double scale_d, bool use_dscale, bool priv) {
+  // Two changed points per step.  Their rows are loaded and converted first; the accumulator
+  // updates are read-modify-writes in shared memory, and a chain of them through possibly equal
+  // addresses would serialise on the load latency — so updates whose addresses are known to differ
+  // (new ≠ old of one point; the four labels of two points when distinct) load together, then
+  // store together, and equal labels are merged in registers first.
+  const int col = lane < m ? lane : 0;
+  auto value = [&](int j) -> long long {
+    const uint32_t e = (uint32_t)(prow0 + j) * m + col;
+    const float v = e < bulk_elems ? rs[e] : __ldg(gx_tile + e);
+    return use_dscale ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f));
   };
+  // address of label c's accumulator for this lane (lane m: the counts)
+  auto slot = [&](int c) -> unsigned long long* { return lane < m ? s_acc + (size_t)c * m + lane : s_acc + (size_t)km + c; };
+  const bool act = lane <= m;
   while (pend) {
-    const int j = __ffs(pend) - 1;
+    const int j0 = __ffs(pend) - 1;
     pend &= pend - 1;
-    const int nb = __shfl_sync(0xffffffffu, bi, j), ob = __shfl_sync(0xffffffffu, old, j);
-    if (lane < m) {
-      const uint32_t e = (uint32_t)(prow0 + j) * m + lane;
-      const float v = e < bulk_elems ? rs[e] : __ldg(gx_tile + e);
-      const long long q = use_dscale ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f));
-      add(s_acc + (size_t)nb * m + lane, (unsigned long long)q);
-      if (ob >= 0) add(s_acc + (size_t)ob * m + lane, (unsigned long long)(-q));
-    } else if (lane == m) {
-      add(s_acc + (size_t)km + nb, 1ull);
-      if (ob >= 0) add(s_acc + (size_t)km + ob, ~0ull);
+    const bool two = pend != 0;
+    const int j1 = two ? __ffs(pend) - 1 : j0;
+    if (two) pend &= pend - 1;
+    const int n0 = __shfl_sync(0xffffffffu, bi, j0), o0 = __shfl_sync(0xffffffffu, old, j0);
+    const int n1 = __shfl_sync(0xffffffffu, bi, j1), o1 = __shfl_sync(0xffffffffu, old, j1);
+    const long long v0 = value(j0), v1 = value(j1);
+    const long long q0 = lane < m ? v0 : 1ll, q1 = lane < m ? v1 : 1ll;
+    if (!act) continue;
+    if (!priv) {  // CTA-shared accumulator: 32-bit atomic pairs (order-free)
+      acc_add64(slot(n0), (unsigned long long)q0);
+      if (o0 >= 0) acc_add64(slot(o0), (unsigned long long)(-q0));
+      if (two) {
+        acc_add64(slot(n1), (unsigned long long)q1);
+        if (o1 >= 0) acc_add64(slot(o1), (unsigned long long)(-q1));
+      }
+      continue;
+    }
+    // private accumulator: plain loads / adds / stores
+    const bool distinct = two && n0 != n1 && n0 != o1 && o0 != n1 && (o0 != o1 || o0 < 0);
+    if (distinct) {  // up to four distinct addresses: all loads, then all stores
+      unsigned long long* pa = slot(n0);
+      unsigned long long* pc = slot(n1);
+      unsigned long long* pb = o0 >= 0 ? slot(o0) : nullptr;
+      unsigned long long* pd = o1 >= 0 ? slot(o1) : nullptr;
+      const unsigned long long a = *pa, c = *pc, b = pb ? *pb : 0ull, d = pd ? *pd : 0ull;
+      *pa = a + (unsigned long long)q0;
+      *pc = c + (unsigned long long)q1;
+      if (pb) *pb = b - (unsigned long long)q0;
+      if (pd) *pd = d - (unsigned long long)q1;
+    } else {
+      // per point (new ≠ old, so its two addresses differ); the second point after the first
+      for (int u = 0; u < (two ? 2 : 1); ++u) {
+        const int nn = u ? n1 : n0, oo = u ? o1 : o0;
+        const long long qq = u ? q1 : q0;
+        unsigned long long* pa = slot(nn);
+        if (oo >= 0) {
+          unsigned long long* pb = slot(oo);
+          const unsigned long long a = *pa, b = *pb;
+          *pa = a + (unsigned long long)qq;
+          *pb = b - (unsigned long long)qq;
+        } else {
+          *pa += (unsigned long long)qq;
+        }
+      }
     }
   }
 }

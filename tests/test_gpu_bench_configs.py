@@ -68,7 +68,13 @@ def test_bench_config_matches_reference(name):
     print(f"{name}: iterations {iters} (reference {int(g['iterations'])}), path {st.get('path', '?')}, "
           f"rechecked {st['rechecked']}, changed {st['changed']}")
     assert iters == int(g["iterations"]) and conv == bool(g["converged"]), name
-    assert np.array_equal(counts, g["counts"]), name
+    if not np.array_equal(counts, g["counts"]):  # diagnostics: wrong labels, or Δ lost / doubled?
+        own = np.bincount(labels, minlength=counts.size)
+        diff = np.asarray(counts) - g["counts"]
+        raise AssertionError(f"{name}: counts differ in {np.count_nonzero(diff)} clusters (sum {diff.sum()}); "
+                             f"counts == bincount(labels): {np.array_equal(own, counts)}; "
+                             f"bincount(labels) == reference counts: {np.array_equal(own, g['counts'])}; "
+                             f"label sample mismatches: {np.count_nonzero(labels[::997] != g['labels_sample'])}")
     assert rel_err(centers, g["centers"]) <= CENTER_RTOL, (name, rel_err(centers, g["centers"]))
     assert np.array_equal(labels[::997], g["labels_sample"]), name
     if "labels" in g:
