@@ -597,6 +597,51 @@ __device__ __forceinline__ int exact_candidates(const T* __restrict__ gx, int m,
 //    adds it to the new cluster / subtracts it from the old one; lane m moves the counts;
 //  * the first pass (every point adds its row): thread per point, loads batched ahead of the
 //    atomics.
+// Δ of up to two changed points into a warp's accumulator row of this lane (slot(c): label c's
+// word).  Read-modify-writes through possibly equal addresses would serialise on the shared-memory
+// load latency, so updates whose addresses are known to differ — new ≠ old of one point; the four
+// labels of two points when distinct — load together, then store together.  !priv: the CTA-shared
+// accumulator, 32-bit atomic pairs (order-free).
+template <typename Slot>
+__device__ __forceinline__ void acc_apply2(Slot slot, bool priv, bool two, int n0, int o0, long long q0, int n1, int o1,
+                                           long long q1) {
+  if (!priv) {
+    acc_add64(slot(n0), (unsigned long long)q0);
+    if (o0 >= 0) acc_add64(slot(o0), (unsigned long long)(-q0));
+    if (two) {
+      acc_add64(slot(n1), (unsigned long long)q1);
+      if (o1 >= 0) acc_add64(slot(o1), (unsigned long long)(-q1));
+    }
+    return;
+  }
+  const bool distinct = two && n0 != n1 && n0 != o1 && o0 != n1 && (o0 != o1 || o0 < 0);
+  if (distinct) {
+    unsigned long long* pa = slot(n0);
+    unsigned long long* pc = slot(n1);
+    unsigned long long* pb = o0 >= 0 ? slot(o0) : nullptr;
+    unsigned long long* pd = o1 >= 0 ? slot(o1) : nullptr;
+    const unsigned long long a = *pa, c = *pc, b = pb ? *pb : 0ull, d = pd ? *pd : 0ull;
+    *pa = a + (unsigned long long)q0;
+    *pc = c + (unsigned long long)q1;
+    if (pb) *pb = b - (unsigned long long)q0;
+    if (pd) *pd = d - (unsigned long long)q1;
+    return;
+  }
+  for (int u = 0; u < (two ? 2 : 1); ++u) {  // per point (its two addresses differ), in order
+    const int nn = u ? n1 : n0, oo = u ? o1 : o0;
+    const long long qq = u ? q1 : q0;
+    unsigned long long* pa = slot(nn);
+    if (oo >= 0) {
+      unsigned long long* pb = slot(oo);
+      const unsigned long long a = *pa, b = *pb;
+      *pa = a + (unsigned long long)qq;
+      *pb = b - (unsigned long long)qq;
+    } else {
+      *pa += (unsigned long long)qq;
+    }
+  }
+}
+
 template <bool X64>
 static __device__ __noinline__ void delta_rows(const float* __restrict__ x, const double* __restrict__ x64, int m,
                                         int64_t wrow0, int lane, int bi, int old,
@@ -609,9 +654,6 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, cons
     return use_dscale ? __double2ll_rn(__dmul_rn((double)v, scale_d)) : __float2ll_rn(__fmul_rn(v, scale_f));
   };
   // priv: s_acc is this warp's private accumulator — the lane-per-feature path adds without atomics
-  auto add = [&](unsigned long long* p, unsigned long long v) {
-    if (priv) *p += v; else acc_add64(p, v);
-  };
   if (full) {
     if (!((pend >> lane) & 1u)) return;
     constexpr int CH = 8;
@@ -632,29 +674,19 @@ static __device__ __noinline__ void delta_rows(const float* __restrict__ x, cons
     if (old >= 0) acc_add64(s_acc + (size_t)km + old, ~0ull);
     return;
   }
+  // sparse: two changed points per step; lane f loads feature f of both rows (L2), lane m counts
+  auto slot = [&](int c) -> unsigned long long* { return lane < m ? s_acc + (size_t)c * m + lane : s_acc + (size_t)km + c; };
   while (pend) {
-    int src[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      src[j] = pend ? __ffs(pend) - 1 : -1;
-      if (pend) pend &= pend - 1;
-    }
-    long long qv[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) qv[j] = (src[j] >= 0 && lane < m) ? ldq(wrow0 + src[j], lane) : 0ll;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      if (src[j] < 0) break;
-      const int nb = __shfl_sync(0xffffffffu, bi, src[j]), ob = __shfl_sync(0xffffffffu, old, src[j]);
-      if (lane < m) {
-        const long long v = qv[j];
-        add(s_acc + (size_t)nb * m + lane, (unsigned long long)v);
-        if (ob >= 0) add(s_acc + (size_t)ob * m + lane, (unsigned long long)(-v));
-      } else if (lane == m) {
-        add(s_acc + (size_t)km + nb, 1ull);
-        if (ob >= 0) add(s_acc + (size_t)km + ob, ~0ull);
-      }
-    }
+    const int j0 = __ffs(pend) - 1;
+    pend &= pend - 1;
+    const bool two = pend != 0;
+    const int j1 = two ? __ffs(pend) - 1 : j0;
+    if (two) pend &= pend - 1;
+    const int n0 = __shfl_sync(0xffffffffu, bi, j0), o0 = __shfl_sync(0xffffffffu, old, j0);
+    const int n1 = __shfl_sync(0xffffffffu, bi, j1), o1 = __shfl_sync(0xffffffffu, old, j1);
+    const long long q0 = lane < m ? ldq(wrow0 + j0, lane) : 1ll;
+    const long long q1 = lane < m && two ? ldq(wrow0 + j1, lane) : 1ll;
+    if (lane <= m) acc_apply2(slot, priv, two, n0, o0, q0, n1, o1, q1);
   }
 }
 
@@ -667,11 +699,7 @@ static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__
                                                        int bi, int old, unsigned int pend,
                                                        unsigned long long* __restrict__ s_acc, int km, float scale_f,
                                                        double scale_d, bool use_dscale, bool priv) {
-  // Two changed points per step.  Their rows are loaded and converted first; the accumulator
-  // updates are read-modify-writes in shared memory, and a chain of them through possibly equal
-  // addresses would serialise on the load latency — so updates whose addresses are known to differ
-  // (new ≠ old of one point; the four labels of two points when distinct) load together, then
-  // store together, and equal labels are merged in registers first.
+  // Two changed points per step: rows loaded and converted first, then acc_apply2.
   const int col = lane < m ? lane : 0;
   auto value = [&](int j) -> long long {
     const uint32_t e = (uint32_t)(prow0 + j) * m + col;
@@ -691,44 +719,7 @@ static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__
     const int n1 = __shfl_sync(0xffffffffu, bi, j1), o1 = __shfl_sync(0xffffffffu, old, j1);
     const long long v0 = value(j0), v1 = value(j1);
     const long long q0 = lane < m ? v0 : 1ll, q1 = lane < m ? v1 : 1ll;
-    if (!act) continue;
-    if (!priv) {  // CTA-shared accumulator: 32-bit atomic pairs (order-free)
-      acc_add64(slot(n0), (unsigned long long)q0);
-      if (o0 >= 0) acc_add64(slot(o0), (unsigned long long)(-q0));
-      if (two) {
-        acc_add64(slot(n1), (unsigned long long)q1);
-        if (o1 >= 0) acc_add64(slot(o1), (unsigned long long)(-q1));
-      }
-      continue;
-    }
-    // private accumulator: plain loads / adds / stores
-    const bool distinct = two && n0 != n1 && n0 != o1 && o0 != n1 && (o0 != o1 || o0 < 0);
-    if (distinct) {  // up to four distinct addresses: all loads, then all stores
-      unsigned long long* pa = slot(n0);
-      unsigned long long* pc = slot(n1);
-      unsigned long long* pb = o0 >= 0 ? slot(o0) : nullptr;
-      unsigned long long* pd = o1 >= 0 ? slot(o1) : nullptr;
-      const unsigned long long a = *pa, c = *pc, b = pb ? *pb : 0ull, d = pd ? *pd : 0ull;
-      *pa = a + (unsigned long long)q0;
-      *pc = c + (unsigned long long)q1;
-      if (pb) *pb = b - (unsigned long long)q0;
-      if (pd) *pd = d - (unsigned long long)q1;
-    } else {
-      // per point (new ≠ old, so its two addresses differ); the second point after the first
-      for (int u = 0; u < (two ? 2 : 1); ++u) {
-        const int nn = u ? n1 : n0, oo = u ? o1 : o0;
-        const long long qq = u ? q1 : q0;
-        unsigned long long* pa = slot(nn);
-        if (oo >= 0) {
-          unsigned long long* pb = slot(oo);
-          const unsigned long long a = *pa, b = *pb;
-          *pa = a + (unsigned long long)qq;
-          *pb = b - (unsigned long long)qq;
-        } else {
-          *pa += (unsigned long long)qq;
-        }
-      }
-    }
+    if (act) acc_apply2(slot, priv, two, n0, o0, q0, n1, o1, q1);
   }
 }
 
