@@ -65,13 +65,31 @@ __device__ __forceinline__ void sums_rows_full(const T* __restrict__ sxw, const 
                                                int lane, unsigned long long* acc_lane, float scale_f, double scale_d,
                                                T cnt_v) {
   const bool feat = lane < MT;
+  if (PRIV) {
+    // rows in pairs: the read-modify-writes of two different labels load together, then store
+    // together (one dependent chain per pair instead of per row); equal labels add in registers
 #pragma unroll
-  for (int j = 0; j < RPW; ++j) {
-    const int L = slw[j];
-    const T v = feat ? sxw[j * MT] : cnt_v;
-    const unsigned long long q = (unsigned long long)to_fixed<T>(v, scale_f, scale_d, 0);
-    unsigned long long* dst = acc_lane + L * (MT + 1);
-    if (PRIV) *dst += q; else smem_add64(dst, q);
+    for (int j = 0; j < RPW; j += 2) {
+      const int L0 = slw[j], L1 = slw[j + 1];
+      const unsigned long long q0 = (unsigned long long)to_fixed<T>(feat ? sxw[j * MT] : cnt_v, scale_f, scale_d, 0);
+      const unsigned long long q1 = (unsigned long long)to_fixed<T>(feat ? sxw[(j + 1) * MT] : cnt_v, scale_f, scale_d, 0);
+      unsigned long long* d0 = acc_lane + L0 * (MT + 1);
+      if (L0 != L1) {
+        unsigned long long* d1 = acc_lane + L1 * (MT + 1);
+        const unsigned long long a0 = *d0, a1 = *d1;
+        *d0 = a0 + q0;
+        *d1 = a1 + q1;
+      } else {
+        *d0 += q0 + q1;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < RPW; ++j) {
+      const int L = slw[j];
+      const T v = feat ? sxw[j * MT] : cnt_v;
+      smem_add64(acc_lane + L * (MT + 1), (unsigned long long)to_fixed<T>(v, scale_f, scale_d, 0));
+    }
   }
 }
 
