@@ -103,7 +103,7 @@ struct km_engine {
   int32_t path_pref = 0;            // 0 auto, 1 SIMT only, 2 tensor-core required, 3 SIMT without register blocking
   float* dbg_scores = nullptr;      // test hook: raw tensor-core scores
   // environment knobs, read once at km_create (tuning / A-B experiments only)
-  bool full_first_pass = false;     // KM_FULL_FIRST_PASS=1: fused full first pass (epilogue atomics)
+  int full_first_pass = -1;         // KM_FULL_FIRST_PASS=1 / 0: force the fused / split first pass (-1: by n)
   bool no_resident = false;         // KM_NO_RESIDENT=1: launch-per-iteration loop
   bool call_trace = false;          // KM_CALL_TRACE=1: per-step device/host times of km_lloyd (stderr)
   int dbg_flags = 0;                // KM_TC_DBG
@@ -943,7 +943,7 @@ int km_create(int32_t device, km_engine** out) {
                    prop.major, prop.minor);
   km_engine* e = new km_engine();
   e->device = device;
-  e->full_first_pass = getenv("KM_FULL_FIRST_PASS") && atoi(getenv("KM_FULL_FIRST_PASS")) != 0;
+  e->full_first_pass = getenv("KM_FULL_FIRST_PASS") ? (atoi(getenv("KM_FULL_FIRST_PASS")) != 0 ? 1 : 0) : -1;
   e->no_resident = getenv("KM_NO_RESIDENT") != nullptr;
   e->call_trace = getenv("KM_CALL_TRACE") != nullptr;
   e->no_shadow = getenv("KM_NO_FP32_SHADOW") != nullptr;
@@ -1247,9 +1247,12 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
   }
   // First pass split in two: L0 = A(C0) writes labels only (tensor cores), then one cluster-sums
   // stream adds every point to its cluster (S(L0) into tot); the resident loop starts at the
-  // finish of iteration 1.  (KM_FULL_FIRST_PASS=1: the fused first pass adding every point
-  // through the epilogue's shared-memory atomics, kept for A/B timing.)
-  const bool split = !e->full_first_pass || e->peer_active;  // (the peer loop exchanges the split's local sums)
+  // finish of iteration 1.  Small point sets take the fused full first pass inside the resident
+  // launch instead (two launches fewer: cfg1 9.2 → 8.7, cfg2 11.8 → 11.4 µs per step; at cfg3 the
+  // split is 85 µs per call faster).  KM_FULL_FIRST_PASS=1 / 0 forces either (A/B timing).
+  constexpr int64_t kSplitFirstMinRows = 500000;
+  const bool split = e->peer_active ||  // (the peer loop exchanges the split's local sums)
+                     (e->full_first_pass < 0 ? e->n >= kSplitFirstMinRows : e->full_first_pass == 0);
   bool full = !split && !resume, first = !resume;
   DevState* hs = e->st_host;
   for (;;) {
