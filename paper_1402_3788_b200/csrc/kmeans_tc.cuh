@@ -76,6 +76,12 @@ constexpr int kMmaWarp = kProducerWarp + 1;                 // TMEM allocator + 
 constexpr int kMmaWarps = 2;                                // issuers: tile g → warp kMmaWarp + g % 2
 constexpr int kRecheckWarp = kMmaWarp + kMmaWarps;          // exact re-decision of queued points, during the pass
 constexpr int kThreadsTC = (kRecheckWarp + 1) * 32;
+// tail of a run-ahead pass boundary: every warp but the transform groups and the producer
+constexpr int kTailThreads = kThreadsTC - (kTransformWarps + 1) * 32;
+constexpr int kTailBar = 14;  // named barrier of those warps
+#ifndef KM_RUN_AHEAD
+#define KM_RUN_AHEAD 1
+#endif
 // Ring depths and tile height.  The pass is HBM bound: the raw ring (TMA → transform) gets the
 // shared memory the other sections leave (~64 KB in flight per SM covers the loaded DRAM
 // latency).  Tiles of 256 points (two M=128 MMA blocks) halve every per-tile handshake per
@@ -853,6 +859,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   // Heavy passes (many label changes): the raw tile stays until the epilogue, which takes the
   // changed points' rows from shared memory.  Decided per CTA from its previous pass's changes
   // (the first pass after a separate L0 pass, and full first passes, are heavy).
+  __shared__ int s_tail[5];  // run-ahead: loop state published by the tail for the warps that skipped it
   __shared__ int s_heavy;
   __shared__ unsigned int s_pass_changes;
   if (tid == 0) {
@@ -864,6 +871,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   int cb = 0;      // resident: s_cbuf half holding C_t
   int g0 = 0;      // tiles of earlier passes (ring positions continue across passes)
   int issued = 0;  // producer: tiles of the current pass already in flight
+  int pre_done = 0;  // transform: tiles of the current pass transformed ahead (in the last tail)
   int last_pass_tiles = my_tiles;
 
   // tuning only: per-pass phase ends (globaltimer, max over CTAs) of the resident loop
@@ -945,6 +953,131 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       }
       s_q[q] = 0;  // free for the next pass
     };
+    // TMA producer: tile g (index i of its pass) → raw slot g % RS (one thread); also issued ahead in the tail
+    const uint64_t pol = l2_policy_evict_first();
+    auto issue = [&](int g, int i) {
+      const int s = g % RS;
+      if (g >= RS) mbar_wait(empty_raw + s, ((g / RS) - 1) & 1);
+      const int64_t row0 = (t_lo + i) * TR;
+      const int64_t rem = a.n - row0;
+      const int rows = rem < TR ? (int)rem : TR;
+      const uint32_t bytes = ((uint32_t)rows * m * 4u) & ~15u;
+      mbar_arrive_expect_tx(full_raw + s, bytes);
+      if (bytes)
+        bulk_g2s_hint(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes, full_raw + s, pol);
+    };
+    // transform of tile g (index i of its pass): raw rows → the A operand; hv: heavy pass (the
+    // epilogue, not the transform, releases the raw slot).  Also run ahead in the tail (below).
+    const int tg = warp >> 2;
+    const int p_t = tid & 127;
+    auto transform_tile = [&](const int g, const int i, const bool hv) {
+      const int p = p_t;
+      const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
+      const int key = p & 7;
+      const float* __restrict__ gx = a.x;
+        const int s = g % RS, sa = g % AS;
+        const int64_t row0 = (t_lo + i) * TR;
+        const int64_t rem = a.n - row0;
+        const int rows = rem < TR ? (int)rem : TR;
+        const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
+        long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
+        if (stamp) ts[0] = clock64();
+        if (KM_GROUP_WAIT & 2) {  // one warp of the group polls both barriers, the other three park in bar.sync
+          if ((warp & 3) == 0) {
+            mbar_wait(full_raw + s, (g / RS) & 1);
+            if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+          }
+          named_bar_sync(1 + kEpiGroups + tg, 128);
+          tc_fence_after();
+        } else {
+          mbar_wait(full_raw + s, (g / RS) & 1);
+        }
+        if (stamp) ts[1] = clock64();
+        if (KM_DBG_FLAGS & 4) {  // tuning only: measure the TMA stream alone
+          __syncwarp();
+          if (lane == 0) mbar_arrive(empty_raw + s);
+          return;
+        }
+        const float* rs = raw + s * (S.raw_stride / 4);
+        if (!(KM_GROUP_WAIT & 2) && g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
+        if (stamp) ts[7] = clock64();
+        unsigned char* s_a = sm + S.off_a + sa * (TR * 128);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {  // thread = points p and p + 128 (tall tiles)
+          const int pp = p + 128 * mb;
+          const bool active = pp < rows;
+          float xs[L::HW];
+          if (KM_DBG_FLAGS & 512) {  // timing experiment only: no raw-tile loads
+#pragma unroll
+            for (int f = 0; f < L::HW; ++f) xs[f] = 0.f;
+          } else if (rows == TR) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
+            const float* xr = rs + pp * m;
+#pragma unroll
+            for (int f = 0; f < L::HW; ++f) {
+              const float v = (f < MP) ? xr[f] : 0.f;
+              xs[f] = (f < m) ? (PRE ? v * pre : v) : 0.f;
+            }
+          } else {  // ragged last tile: bulk part + ≤ 3 trailing floats from global
+            const uint32_t bulk_elems = (((uint32_t)rows * m * 4u) & ~15u) >> 2;
+            for (int f = 0; f < L::HW; ++f) {
+              float v = 0.f;
+              if (f < MP && f < m && active) {
+                const uint32_t e = (uint32_t)pp * m + f;
+                v = ((e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e));
+                if (PRE) v *= pre;
+              }
+              xs[f] = v;
+            }
+          }
+#pragma unroll
+          for (int f = 0; f < L::HW; ++f)
+            if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
+          uint32_t hw[L::HW / 2], lw[L::HW / 2];
+#pragma unroll
+          for (int q = 0; q < L::HW / 2; ++q) {
+            if (KM_DBG_FLAGS & 512) {  // timing experiment only: no transform arithmetic
+              hw[q] = lw[q] = 0u;
+              continue;
+            }
+            const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
+            const float2 hf = __half22float2(h2);
+            // x − fl(xh) for both lanes in one packed FADD2
+            const float2 d = __fadd2_rn(make_float2(xs[2 * q], xs[2 * q + 1]), make_float2(-hf.x, -hf.y));
+            const __half2 l2 = __floats2half2_rn(d.x, d.y);
+            hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
+            lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
+          }
+          if constexpr (TS) {
+            // the point's A row [xh | xl] (HW 32-bit columns) → TMEM lane p of this tile's A buffer
+            const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + TM::a_base + (uint32_t)(sa * TM::arow);
+            tmem_st_row<L::HW / 2>(ta, hw);             // [xh | xl]
+            tmem_st_row<L::HW / 2>(ta + L::HW / 2, lw);
+          } else {
+            unsigned char* s_ab = s_a + mb * (128 * 128);
+#pragma unroll
+            for (int q = 0; q < L::HW / 8; ++q) {
+              *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)(q ^ key) << 4)) =
+                  make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
+              *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
+                  make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
+            }
+          }
+        }
+        // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
+        // the TMA producer may refill it (heavy passes: the epilogue releases it)
+        __syncwarp();
+        if (lane == 0 && !hv) mbar_arrive(empty_raw + s);
+        if (stamp) ts[2] = clock64();
+        if constexpr (TS) {
+          tmem_st_wait();      // the A row is in TMEM
+          tc_fence_before();   // ordered before the hand-off to the MMA issuer
+        } else {
+          fence_proxy_async();  // generic-proxy A stores → visible to the tensor core
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full + sa);
+        if (stamp) ts[3] = clock64();
+    };
     if (warp == kRecheckWarp) {
       // ===================== recheck warp: re-decides queued points while the pass streams =====================
       unsigned int done = 0;
@@ -975,19 +1108,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     } else if (warp == kProducerWarp) {
       // ===================== TMA producer: tile g → raw slot g % RS =====================
       if (lane == 0) {
-        const uint64_t pol = l2_policy_evict_first();
-        auto issue = [&](int g, int i) {
-          const int s = g % RS;
-          if (g >= RS) mbar_wait(empty_raw + s, ((g / RS) - 1) & 1);
-          const int64_t row0 = (t_lo + i) * TR;
-          const int64_t rem = a.n - row0;
-          const int rows = rem < TR ? (int)rem : TR;
-          const uint32_t bytes = ((uint32_t)rows * m * 4u) & ~15u;
-          mbar_arrive_expect_tx(full_raw + s, bytes);
-          if (bytes)
-            bulk_g2s_hint(reinterpret_cast<unsigned char*>(raw) + s * S.raw_stride, a.x + row0 * m, bytes, full_raw + s,
-                          pol);
-        };
         for (int i = issued; i < pass_tiles; ++i) issue(g0 + i, i);
         for (int j = 0; j < npre; ++j) issue(g0 + pass_tiles + j, j);  // next pass (resident)
       }
@@ -1060,117 +1180,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       }
     } else if (warp < kTransformWarps) {
       // ===================== transform: thread = point; group tg takes tiles g ≡ tg (mod 2) =====================
-      const int tg = warp >> 2;
-      const int p = tid & 127;
-      const uint32_t row_off = (uint32_t)((p >> 3) * 1024 + (p & 7) * 128);  // SW128 geometry of row p
-      const int key = p & 7;
-      const float* __restrict__ gx = a.x;
+      // (tiles below pre_done were transformed during the previous pass's tail)
       for (int i = ((tg - g0) % kTransformGroups + kTransformGroups) % kTransformGroups; i < pass_tiles;
-           i += kTransformGroups) {
-        const int g = g0 + i;
-        const int s = g % RS, sa = g % AS;
-        const int64_t row0 = (t_lo + i) * TR;
-        const int64_t rem = a.n - row0;
-        const int rows = rem < TR ? (int)rem : TR;
-        const bool stamp = KM_TC_TUNING && a.dbg_times != nullptr && blockIdx.x == 0 && p == 0 && i < 64 && it == (resident ? 100 : 0);
-        long long* ts = stamp ? a.dbg_times + (size_t)i * 8 : nullptr;
-        if (stamp) ts[0] = clock64();
-        if (KM_GROUP_WAIT & 2) {  // one warp of the group polls both barriers, the other three park in bar.sync
-          if ((warp & 3) == 0) {
-            mbar_wait(full_raw + s, (g / RS) & 1);
-            if (g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
-          }
-          named_bar_sync(1 + kEpiGroups + tg, 128);
-          tc_fence_after();
-        } else {
-          mbar_wait(full_raw + s, (g / RS) & 1);
-        }
-        if (stamp) ts[1] = clock64();
-        if (KM_DBG_FLAGS & 4) {  // tuning only: measure the TMA stream alone
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty_raw + s);
-          continue;
-        }
-        const float* rs = raw + s * (S.raw_stride / 4);
-        if (!(KM_GROUP_WAIT & 2) && g >= AS) mbar_wait(a_empty + sa, ((g / AS) - 1) & 1);  // this group's A buffer is free
-        if (stamp) ts[7] = clock64();
-        unsigned char* s_a = sm + S.off_a + sa * (TR * 128);
-#pragma unroll
-        for (int mb = 0; mb < MB; ++mb) {  // thread = points p and p + 128 (tall tiles)
-          const int pp = p + 128 * mb;
-          const bool active = pp < rows;
-          float xs[L::HW];
-          if (KM_DBG_FLAGS & 512) {  // timing experiment only: no raw-tile loads
-#pragma unroll
-            for (int f = 0; f < L::HW; ++f) xs[f] = 0.f;
-          } else if (rows == TR) {  // full tile: branch-free loads (over-reads stay inside the padded slot)
-            const float* xr = rs + pp * m;
-#pragma unroll
-            for (int f = 0; f < L::HW; ++f) {
-              const float v = (f < MP) ? xr[f] : 0.f;
-              xs[f] = (f < m) ? (PRE ? v * pre : v) : 0.f;
-            }
-          } else {  // ragged last tile: bulk part + ≤ 3 trailing floats from global
-            const uint32_t bulk_elems = (((uint32_t)rows * m * 4u) & ~15u) >> 2;
-            for (int f = 0; f < L::HW; ++f) {
-              float v = 0.f;
-              if (f < MP && f < m && active) {
-                const uint32_t e = (uint32_t)pp * m + f;
-                v = ((e < bulk_elems) ? rs[e] : __ldg(gx + row0 * m + e));
-                if (PRE) v *= pre;
-              }
-              xs[f] = v;
-            }
-          }
-#pragma unroll
-          for (int f = 0; f < L::HW; ++f)
-            if (f == m) xs[f] = active ? 1.f : 0.f;  // ones column picks up ‖c‖²
-          uint32_t hw[L::HW / 2], lw[L::HW / 2];
-#pragma unroll
-          for (int q = 0; q < L::HW / 2; ++q) {
-            if (KM_DBG_FLAGS & 512) {  // timing experiment only: no transform arithmetic
-              hw[q] = lw[q] = 0u;
-              continue;
-            }
-            const __half2 h2 = __floats2half2_rn(xs[2 * q], xs[2 * q + 1]);
-            const float2 hf = __half22float2(h2);
-            // x − fl(xh) for both lanes in one packed FADD2
-            const float2 d = __fadd2_rn(make_float2(xs[2 * q], xs[2 * q + 1]), make_float2(-hf.x, -hf.y));
-            const __half2 l2 = __floats2half2_rn(d.x, d.y);
-            hw[q] = *reinterpret_cast<const uint32_t*>(&h2);
-            lw[q] = *reinterpret_cast<const uint32_t*>(&l2);
-          }
-          if constexpr (TS) {
-            // the point's A row [xh | xl] (HW 32-bit columns) → TMEM lane p of this tile's A buffer
-            const uint32_t ta = tmem + ((uint32_t)((warp & 3) * 32) << 16) + TM::a_base + (uint32_t)(sa * TM::arow);
-            tmem_st_row<L::HW / 2>(ta, hw);             // [xh | xl]
-            tmem_st_row<L::HW / 2>(ta + L::HW / 2, lw);
-          } else {
-            unsigned char* s_ab = s_a + mb * (128 * 128);
-#pragma unroll
-            for (int q = 0; q < L::HW / 8; ++q) {
-              *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)(q ^ key) << 4)) =
-                  make_uint4(hw[4 * q], hw[4 * q + 1], hw[4 * q + 2], hw[4 * q + 3]);
-              *reinterpret_cast<uint4*>(s_ab + row_off + ((uint32_t)((q + L::HW / 8) ^ key) << 4)) =
-                  make_uint4(lw[4 * q], lw[4 * q + 1], lw[4 * q + 2], lw[4 * q + 3]);
-            }
-          }
-        }
-        // raw slot consumed (every loaded value has been used, so no LDS is still in flight):
-        // the TMA producer may refill it (heavy passes: the epilogue releases it)
-        __syncwarp();
-        if (lane == 0 && !heavy) mbar_arrive(empty_raw + s);
-        if (stamp) ts[2] = clock64();
-        if constexpr (TS) {
-          tmem_st_wait();      // the A row is in TMEM
-          tc_fence_before();   // ordered before the hand-off to the MMA issuer
-        } else {
-          fence_proxy_async();  // generic-proxy A stores → visible to the tensor core
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(a_full + sa);
-        if (stamp) ts[3] = clock64();
-      }
+           i += kTransformGroups)
+        if (i >= pre_done) transform_tile(g0 + i, i, heavy);
     } else {
       // ===================== epilogue groups: thread = point = TMEM lane; group e takes tiles g ≡ e (mod 2) =====================
       const int ew = warp - kTransformWarps;  // 0..7
@@ -1408,244 +1421,292 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
     if (pst && (it == 100 || it == 101 || it == 150))
       a.dbg_times[6144 + (it == 100 ? 0 : it == 101 ? 300 : 600) + blockIdx.x * 2 + 1] = (long long)globaltimer();
-    double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
-    const int stage_cap = (int)(RS * S.raw_stride / 8);
-    {
-      // queue entries the recheck warp had not reached when the pass ended: thread per point
-      const unsigned int qn = min(s_qn[0], (unsigned int)QCAP);
-      for (unsigned int q = s_qn[2] + tid; q < qn; q += kThreadsTC) redecide(q, s_q[q]);
-      __syncthreads();
-      if (PD) {  // the epilogue warps' private Δ into the CTA's accumulator (and cleared for the next pass)
-        for (int i = tid; i < nacc; i += kThreadsTC) {
-          unsigned long long v = 0ull;
-#pragma unroll 4
-          for (int w = 0; w < kEpiWarps; ++w) {
-            v += s_pacc[w * PST + i];
-            s_pacc[w * PST + i] = 0ull;
-          }
-          s_acc[i] += v;
-        }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        s_qn[0] = 0u;
-        s_qn[1] = 0u;
-        s_qn[2] = 0u;
-      }
-      if (pst && it < 256) atomicMax(pst + it * 8 + 2, globaltimer());
-    }
-    if (!resident) {
-      for (int i = tid; i < nacc; i += kThreadsTC) {  // one flush of the CTA's Δ
-        const unsigned long long v = s_acc[i];
-        if (v) atomicAdd(a.part + i, v);
-      }
-      if (a.fuse_finish) {
-        // the last CTA to arrive runs the finish of this iteration (no separate launch)
-        __shared__ int s_last;
-        __threadfence();
-        __syncthreads();
-        if (tid == 0) s_last = atomicAdd(a.cta_done, 1u) == gridDim.x - 1;
-        __syncthreads();
-        if (s_last) {
-          __threadfence();
-          finish_block(a.fin, s_stage, stage_cap);
-          if (tid == 0) *a.cta_done = 0u;
-        }
-      }
-      break;
-    }
-    // ---- resident: Δ → the pass's global delta buffer, grid barrier ----
-    // Three delta buffers rotate: pass it accumulates into dlt[it % 3]; before arriving, CTA 0
-    // clears dlt[(it + 1) % 3] — last read in the finish of pass it − 2, which every CTA completed
-    // before it arrived at barrier it − 1 — so no CTA ever waits for the others to finish reading.
-    unsigned long long* dlt = a.dlt + (size_t)(it % 3) * nacc;
-    for (int i = tid; i < nacc; i += kThreadsTC) {
-      const unsigned long long v = s_acc[i];
-      if (v) atomicAdd(dlt + i, v);
-      s_acc[i] = 0ull;
-    }
-    if (blockIdx.x == 0) {
-      unsigned long long* nxt = a.dlt + (size_t)((it + 1) % 3) * nacc;
-      for (int i = tid; i < nacc; i += kThreadsTC) nxt[i] = 0ull;
-    }
-    // grid barrier (the cooperative-groups pattern): the CTA's writes are ordered before thread
-    // 0's gpu-scope fence by the CTA barrier, so one fence per CTA (not one per thread) releases them
-    __syncthreads();
-    if (pst && it < 256) atomicMax(pst + it * 8 + 3, globaltimer());
-    if (pst && it < 256) atomicMax(pst + it * 8 + 4, globaltimer());
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(a.grid_sync, 1u);
-      grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
-    }
-    __syncthreads();
-    if (a.xch_peers != nullptr) {
-      // ---- row-sharded multi-GPU: exchange this iteration's Δ with every rank over NVLink ----
-      // CTA 0 pushes the rank's complete Δ (the local grid barrier has passed) into slot
-      // t_upd & 1, row `rank`, of every rank's buffer, then releases a sequence flag there; every
-      // CTA of every rank waits for all `world` flags and adds the world rows (exact integers, the
-      // same sum on every rank).  Slots alternate: a rank can be at most one exchange ahead (it
-      // needs this rank's next flag to pass the next exchange), so a slot is never overwritten
-      // while it is being read.
-      const int W = a.world;
-      const size_t slot_words = (size_t)W * nacc;
-      const int slot = t_upd & 1;
-      const unsigned long long seq = ((unsigned long long)a.epoch << 32) | (unsigned long long)(unsigned)(t_upd + 1);
-      if (blockIdx.x == 0) {
-        const bool add_local_sums = it == 0 && a.skip_first;
-        for (int pr = 0; pr < W; ++pr) {
-          unsigned long long* dst = a.xch_peers[pr] + slot * slot_words + (size_t)a.rank * nacc;
-          for (int i = tid; i < nacc; i += kThreadsTC)
-            dst[i] = __ldcg(dlt + i) + (add_local_sums ? a.fin.tot[i] : 0ull);
-        }
-        __threadfence_system();
-        __syncthreads();
-        if (tid < W) {
-          unsigned long long* flag = a.xch_peers[tid] + 2 * slot_words + slot * W + a.rank;
-          asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
-        }
-      }
-      if (tid < W) {  // bounded wait (a rank that never arrives traps instead of hanging the GPU)
-        const unsigned long long* flag = a.xch_local + 2 * slot_words + slot * W + tid;
-        const long long t0 = clock64();
-        for (;;) {
-          unsigned long long v;
-          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
-          if (v >= seq) break;
-          if (clock64() - t0 > (1ll << 35)) __trap();
-        }
-      }
-      __syncthreads();
-      const unsigned long long* rows = a.xch_local + slot * slot_words;
-      for (int i = tid; i < nacc; i += kThreadsTC) {
-        unsigned long long d = 0;
-        for (int r = 0; r < W; ++r) d += __ldcg(rows + (size_t)r * nacc + i);
-        const unsigned long long v = s_tot[i] + d;
-        s_tot[i] = v;
-        if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
-      }
-    } else {
-      // running totals of the current labels, per CTA: S_t = S_{t−1} + Δ_t (exact int64)
-      for (int i = tid; i < nacc; i += kThreadsTC) {
-        const unsigned long long v = s_tot[i] + __ldcg(dlt + i);
-        s_tot[i] = v;
-        if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
-      }
-    }
-    __syncthreads();
-    const unsigned long long* tot = s_tot;
-    // ---- resident finish (every CTA; CTA 0 publishes) — engine._finish_update / converged ----
-    const bool pub = blockIdx.x == 0;
+    // Run-ahead (resident, next pass not heavy, not the final pass of an exhausted run): while the
+    // other warps run the tail below (Δ flush, grid barrier, finish, next B operand), the transform
+    // groups convert the next pass's first AS tiles (already prefetched) into the A buffers and the
+    // producer streams the next tiles into the raw slots this frees — the HBM stream and the
+    // transform no longer stop for the tail.  Only tile data moves ahead; nothing depends on C.
+    __syncthreads();  // s_heavy of the next pass, visible to every role
+    const bool ra = KM_RUN_AHEAD && resident && !exhausted && s_heavy == 0 && my_tiles > 0;
+    const bool ra_role = ra && (warp < kTransformWarps || warp == kProducerWarp);
+    // tail threads: all of them, or (run-ahead) every warp but the transform groups and the producer
+    const int ttid = !ra ? tid : warp < kProducerWarp ? tid - kTransformWarps * 32 : tid - (kTransformWarps + 1) * 32;
+    const int tthr = ra ? kTailThreads : kThreadsTC;
+    const int twarp = ttid >> 5;
+    auto tsync = [&]() {
+      if (ra) named_bar_sync(kTailBar, kTailThreads);
+      else __syncthreads();
+    };
     bool stop = false;
-    if (pub && tid == 0 && pass_tiles > 0) st->passes += 1;
-    if (exhausted) {
-      // the final assign pass of an exhausted run: counts = bincount(L_T), C_T unchanged
-      if (pub) {
-        for (int cc = tid; cc < k; cc += kThreadsTC) a.fin.model_counts[cc] = (long long)tot[km + cc];
-        if (tid == 0) st->done = 1;
+    pre_done = 0;
+    if (ra_role) {
+      const int gn = g0 + pass_tiles;        // first tile of the next pass
+      const int pre_n = min(AS, my_tiles);   // transformed ahead (≤ npre: already prefetched)
+      if (warp == kProducerWarp) {
+        if (lane == 0) {  // refill the slots the run-ahead transform releases
+          const int upto = min(npre + pre_n, my_tiles);
+          for (int j = issued; j < upto; ++j) issue(gn + j, j);
+          issued = max(issued, upto);
+        }
+      } else {
+        for (int j = ((tg - gn) % kTransformGroups + kTransformGroups) % kTransformGroups; j < pre_n;
+             j += kTransformGroups)
+          transform_tile(gn + j, j, false);
       }
-      stop = true;
+      pre_done = pre_n;
     } else {
-      double* Cn = s_cbuf + (cb ^ 1) * km;
-      // warp per centre, lane per feature: C_{t+1} = S/N, the congruence terms, ‖fl32(c)‖² and the
-      // centre's two B-operand rows in one pass (no per-centre serial loops on the critical path)
-      __shared__ float s_wmax[32];
-      __shared__ int s_wflags[32];  // bit 0: some cluster empty, bit 1: some centre moved
-      const int hw = 8 * ((m + 1 + 7) / 8);
-      float wmax = 0.f;
-      int wflags = 0;
-      for (int c = warp; c < k; c += kThreadsTC / 32) {
-        const long long nc = (long long)tot[km + c];
-        const bool fv = lane < m;
-        const long long sv = fv ? (long long)tot[(size_t)c * m + lane] : 0ll;
-        // empty clusters get a placeholder; every one is re-seeded by the host repair
-        const double v = (fv && nc > 0) ? __ddiv_rn(__dmul_rn((double)sv, a.fin.inv_scale), (double)nc) : 0.0;
-        const double vo = fv ? C[(size_t)c * m + lane] : 0.0;
-        if (fv) Cn[(size_t)c * m + lane] = v;
+      double* s_stage = reinterpret_cast<double*>(sm + S.off_raw);
+      const int stage_cap = (int)(RS * S.raw_stride / 8);
+      {
+        // queue entries the recheck warp had not reached when the pass ended: thread per point
+        const unsigned int qn = min(s_qn[0], (unsigned int)QCAP);
+        for (unsigned int q = s_qn[2] + ttid; q < qn; q += tthr) redecide(q, s_q[q]);
+        tsync();
+        if (PD) {  // the epilogue warps' private Δ into the CTA's accumulator (and cleared for the next pass)
+          for (int i = ttid; i < nacc; i += tthr) {
+            unsigned long long v = 0ull;
+  #pragma unroll 4
+            for (int w = 0; w < kEpiWarps; ++w) {
+              v += s_pacc[w * PST + i];
+              s_pacc[w * PST + i] = 0ull;
+            }
+            s_acc[i] += v;
+          }
+          tsync();
+        }
+        if (ttid == 0) {
+          s_qn[0] = 0u;
+          s_qn[1] = 0u;
+          s_qn[2] = 0u;
+        }
+        if (pst && it < 256) atomicMax(pst + it * 8 + 2, globaltimer());
+      }
+      if (!resident) {
+        for (int i = ttid; i < nacc; i += tthr) {  // one flush of the CTA's Δ
+          const unsigned long long v = s_acc[i];
+          if (v) atomicAdd(a.part + i, v);
+        }
+        if (a.fuse_finish) {
+          // the last CTA to arrive runs the finish of this iteration (no separate launch)
+          __shared__ int s_last;
+          __threadfence();
+          tsync();
+          if (ttid == 0) s_last = atomicAdd(a.cta_done, 1u) == gridDim.x - 1;
+          tsync();
+          if (s_last) {
+            __threadfence();
+            finish_block(a.fin, s_stage, stage_cap);
+            if (ttid == 0) *a.cta_done = 0u;
+          }
+        }
+        break;
+      }
+      // ---- resident: Δ → the pass's global delta buffer, grid barrier ----
+      // Three delta buffers rotate: pass it accumulates into dlt[it % 3]; before arriving, CTA 0
+      // clears dlt[(it + 1) % 3] — last read in the finish of pass it − 2, which every CTA completed
+      // before it arrived at barrier it − 1 — so no CTA ever waits for the others to finish reading.
+      unsigned long long* dlt = a.dlt + (size_t)(it % 3) * nacc;
+      for (int i = ttid; i < nacc; i += tthr) {
+        const unsigned long long v = s_acc[i];
+        if (v) atomicAdd(dlt + i, v);
+        s_acc[i] = 0ull;
+      }
+      if (blockIdx.x == 0) {
+        unsigned long long* nxt = a.dlt + (size_t)((it + 1) % 3) * nacc;
+        for (int i = ttid; i < nacc; i += tthr) nxt[i] = 0ull;
+      }
+      // grid barrier (the cooperative-groups pattern): the CTA's writes are ordered before thread
+      // 0's gpu-scope fence by the CTA barrier, so one fence per CTA (not one per thread) releases them
+      tsync();
+      if (pst && it < 256) atomicMax(pst + it * 8 + 3, globaltimer());
+      if (pst && it < 256) atomicMax(pst + it * 8 + 4, globaltimer());
+      if (ttid == 0) {
+        __threadfence();
+        atomicAdd(a.grid_sync, 1u);
+        grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
+      }
+      tsync();
+      if (a.xch_peers != nullptr) {
+        // ---- row-sharded multi-GPU: exchange this iteration's Δ with every rank over NVLink ----
+        // CTA 0 pushes the rank's complete Δ (the local grid barrier has passed) into slot
+        // t_upd & 1, row `rank`, of every rank's buffer, then releases a sequence flag there; every
+        // CTA of every rank waits for all `world` flags and adds the world rows (exact integers, the
+        // same sum on every rank).  Slots alternate: a rank can be at most one exchange ahead (it
+        // needs this rank's next flag to pass the next exchange), so a slot is never overwritten
+        // while it is being read.
+        const int W = a.world;
+        const size_t slot_words = (size_t)W * nacc;
+        const int slot = t_upd & 1;
+        const unsigned long long seq = ((unsigned long long)a.epoch << 32) | (unsigned long long)(unsigned)(t_upd + 1);
+        if (blockIdx.x == 0) {
+          const bool add_local_sums = it == 0 && a.skip_first;
+          for (int pr = 0; pr < W; ++pr) {
+            unsigned long long* dst = a.xch_peers[pr] + slot * slot_words + (size_t)a.rank * nacc;
+            for (int i = ttid; i < nacc; i += tthr)
+              dst[i] = __ldcg(dlt + i) + (add_local_sums ? a.fin.tot[i] : 0ull);
+          }
+          __threadfence_system();
+          tsync();
+          if (ttid < W) {
+            unsigned long long* flag = a.xch_peers[ttid] + 2 * slot_words + slot * W + a.rank;
+            asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flag), "l"(seq) : "memory");
+          }
+        }
+        if (ttid < W) {  // bounded wait (a rank that never arrives traps instead of hanging the GPU)
+          const unsigned long long* flag = a.xch_local + 2 * slot_words + slot * W + ttid;
+          const long long t0 = clock64();
+          for (;;) {
+            unsigned long long v;
+            asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flag) : "memory");
+            if (v >= seq) break;
+            if (clock64() - t0 > (1ll << 35)) __trap();
+          }
+        }
+        tsync();
+        const unsigned long long* rows = a.xch_local + slot * slot_words;
+        for (int i = ttid; i < nacc; i += tthr) {
+          unsigned long long d = 0;
+          for (int r = 0; r < W; ++r) d += __ldcg(rows + (size_t)r * nacc + i);
+          const unsigned long long v = s_tot[i] + d;
+          s_tot[i] = v;
+          if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
+        }
+      } else {
+        // running totals of the current labels, per CTA: S_t = S_{t−1} + Δ_t (exact int64)
+        for (int i = ttid; i < nacc; i += tthr) {
+          const unsigned long long v = s_tot[i] + __ldcg(dlt + i);
+          s_tot[i] = v;
+          if (blockIdx.x == 0) a.fin.tot[i] = v;  // published for the host (repair, counts)
+        }
+      }
+      tsync();
+      const unsigned long long* tot = s_tot;
+      // ---- resident finish (every CTA; CTA 0 publishes) — engine._finish_update / converged ----
+      const bool pub = blockIdx.x == 0;
+      if (pub && ttid == 0 && pass_tiles > 0) st->passes += 1;
+      if (exhausted) {
+        // the final assign pass of an exhausted run: counts = bincount(L_T), C_T unchanged
         if (pub) {
-          if (fv) {
-            a.fin.prev[(size_t)c * m + lane] = vo;
-            a.fin.cur[(size_t)c * m + lane] = v;
-          }
-          if (lane == 0) a.fin.model_counts[c] = nc;
-        }
-        // congruence (engine.converged): sqrt(Σ_f (prev − next)², features ascending) ≤ tol
-        const double dd = fv ? __dmul_rn(__dsub_rn(vo, v), __dsub_rn(vo, v)) : 0.0;
-        bool moved;
-        if (tol == 0.0) {
-          moved = __any_sync(0xffffffffu, dd != 0.0);  // a sum of non-negative terms is 0 iff every term is
-        } else {
-          double acc = 0.0;
-          for (int f = 0; f < m; ++f) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, dd, f));
-          moved = !(sqrt(acc) <= tol);
-        }
-        wflags |= (nc == 0 ? 1 : 0) | (moved ? 2 : 0);
-        // filter operand: ‖fl32(c)‖² (fp64, exact squares, fixed tree order), max ‖c‖ rounded up
-        const double q = fv ? (double)__double2float_rn(v) : 0.0;
-        double cn2 = q * q;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) cn2 += __shfl_xor_sync(0xffffffffu, cn2, o);
-        wmax = fmaxf(wmax, __double2float_ru(sqrt(cn2) * (1.0 + 1e-12)));
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int col = lane + 32 * h;
-          const int f = col < hw ? col : col - hw;
-          const double vf = __shfl_sync(0xffffffffu, v, f < 32 ? f : 0);
-          float w = 0.f;
-          if (col < 2 * hw) {
-            if (f < m) w = -2.0f * __double2float_rn(vf) * pre;
-            else if (f == m) w = __double2float_rn(cn2 * (double)pre * (double)pre);
-          }
-          const __half wh = __float2half_rn(w);
-          const __half wl = __float2half_rn(w - __half2float(wh));
-          *reinterpret_cast<unsigned short*>(s_w + sw128(c, col >> 3) + (col & 7) * 2) =
-              (col < 2 * hw) ? __half_as_ushort(wh) : (unsigned short)0;
-          *reinterpret_cast<unsigned short*>(s_w + sw128(KP + c, col >> 3) + (col & 7) * 2) =
-              (col < hw) ? __half_as_ushort(wl) : (unsigned short)0;
-        }
-      }
-      fence_proxy_async();  // B-operand rows → visible to the tensor core after the barrier
-      if (lane == 0) {
-        s_wmax[warp] = wmax;
-        s_wflags[warp] = wflags;
-      }
-      __syncthreads();
-      if (pst && it < 256) atomicMax(pst + it * 8 + 5, globaltimer());
-      int flags = 0;
-      float cmx = 0.f;
-      for (int w = 0; w < kThreadsTC / 32; ++w) {
-        flags |= s_wflags[w];
-        cmx = fmaxf(cmx, s_wmax[w]);
-      }
-      ++t_upd;
-      if (pub && tid == 0) st->t = t_upd;
-      if (flags & 1) {
-        if (pub && tid == 0) {
-          int ne = 0;
-          for (int c = 0; c < k; ++c) ne += (tot[km + c] == 0ull);
-          st->n_empty = ne;
-          st->need_host = 1;
-        }
-        stop = true;
-      } else if (!(flags & 2) && !(KM_DBG_FLAGS & 64)) {  // (dbg 64: timing experiments never converge)
-        if (pub && tid == 0) {
-          st->n_empty = 0;
-          st->converged = 1;
-          st->done = 1;
+          for (int cc = ttid; cc < k; cc += tthr) a.fin.model_counts[cc] = (long long)tot[km + cc];
+          if (ttid == 0) st->done = 1;
         }
         stop = true;
       } else {
-        if (t_upd >= max_iters) {  // reference: one more assign pass, then return
-          exhausted = true;
-          if (pub && tid == 0) st->exhausted = 1;
+        double* Cn = s_cbuf + (cb ^ 1) * km;
+        // warp per centre, lane per feature: C_{t+1} = S/N, the congruence terms, ‖fl32(c)‖² and the
+        // centre's two B-operand rows in one pass (no per-centre serial loops on the critical path)
+        __shared__ float s_wmax[32];
+        __shared__ int s_wflags[32];  // bit 0: some cluster empty, bit 1: some centre moved
+        const int hw = 8 * ((m + 1 + 7) / 8);
+        float wmax = 0.f;
+        int wflags = 0;
+        for (int c = twarp; c < k; c += tthr / 32) {
+          const long long nc = (long long)tot[km + c];
+          const bool fv = lane < m;
+          const long long sv = fv ? (long long)tot[(size_t)c * m + lane] : 0ll;
+          // empty clusters get a placeholder; every one is re-seeded by the host repair
+          const double v = (fv && nc > 0) ? __ddiv_rn(__dmul_rn((double)sv, a.fin.inv_scale), (double)nc) : 0.0;
+          const double vo = fv ? C[(size_t)c * m + lane] : 0.0;
+          if (fv) Cn[(size_t)c * m + lane] = v;
+          if (pub) {
+            if (fv) {
+              a.fin.prev[(size_t)c * m + lane] = vo;
+              a.fin.cur[(size_t)c * m + lane] = v;
+            }
+            if (lane == 0) a.fin.model_counts[c] = nc;
+          }
+          // congruence (engine.converged): sqrt(Σ_f (prev − next)², features ascending) ≤ tol
+          const double dd = fv ? __dmul_rn(__dsub_rn(vo, v), __dsub_rn(vo, v)) : 0.0;
+          bool moved;
+          if (tol == 0.0) {
+            moved = __any_sync(0xffffffffu, dd != 0.0);  // a sum of non-negative terms is 0 iff every term is
+          } else {
+            double acc = 0.0;
+            for (int f = 0; f < m; ++f) acc = __dadd_rn(acc, __shfl_sync(0xffffffffu, dd, f));
+            moved = !(sqrt(acc) <= tol);
+          }
+          wflags |= (nc == 0 ? 1 : 0) | (moved ? 2 : 0);
+          // filter operand: ‖fl32(c)‖² (fp64, exact squares, fixed tree order), max ‖c‖ rounded up
+          const double q = fv ? (double)__double2float_rn(v) : 0.0;
+          double cn2 = q * q;
+  #pragma unroll
+          for (int o = 16; o > 0; o >>= 1) cn2 += __shfl_xor_sync(0xffffffffu, cn2, o);
+          wmax = fmaxf(wmax, __double2float_ru(sqrt(cn2) * (1.0 + 1e-12)));
+  #pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int col = lane + 32 * h;
+            const int f = col < hw ? col : col - hw;
+            const double vf = __shfl_sync(0xffffffffu, v, f < 32 ? f : 0);
+            float w = 0.f;
+            if (col < 2 * hw) {
+              if (f < m) w = -2.0f * __double2float_rn(vf) * pre;
+              else if (f == m) w = __double2float_rn(cn2 * (double)pre * (double)pre);
+            }
+            const __half wh = __float2half_rn(w);
+            const __half wl = __float2half_rn(w - __half2float(wh));
+            *reinterpret_cast<unsigned short*>(s_w + sw128(c, col >> 3) + (col & 7) * 2) =
+                (col < 2 * hw) ? __half_as_ushort(wh) : (unsigned short)0;
+            *reinterpret_cast<unsigned short*>(s_w + sw128(KP + c, col >> 3) + (col & 7) * 2) =
+                (col < hw) ? __half_as_ushort(wl) : (unsigned short)0;
+          }
         }
-        if (tid == 0) s_cmax[0] = cmx;
-        cb ^= 1;
-        full = false;
+        fence_proxy_async();  // B-operand rows → visible to the tensor core after the barrier
+        if (lane == 0) {
+          s_wmax[twarp] = wmax;
+          s_wflags[twarp] = wflags;
+        }
+        tsync();
+        if (pst && it < 256) atomicMax(pst + it * 8 + 5, globaltimer());
+        int flags = 0;
+        float cmx = 0.f;
+        for (int w = 0; w < tthr / 32; ++w) {
+          flags |= s_wflags[w];
+          cmx = fmaxf(cmx, s_wmax[w]);
+        }
+        ++t_upd;
+        if (pub && ttid == 0) st->t = t_upd;
+        if (flags & 1) {
+          if (pub && ttid == 0) {
+            int ne = 0;
+            for (int c = 0; c < k; ++c) ne += (tot[km + c] == 0ull);
+            st->n_empty = ne;
+            st->need_host = 1;
+          }
+          stop = true;
+        } else if (!(flags & 2) && !(KM_DBG_FLAGS & 64)) {  // (dbg 64: timing experiments never converge)
+          if (pub && ttid == 0) {
+            st->n_empty = 0;
+            st->converged = 1;
+            st->done = 1;
+          }
+          stop = true;
+        } else {
+          if (t_upd >= max_iters) {  // reference: one more assign pass, then return
+            exhausted = true;
+            if (pub && ttid == 0) st->exhausted = 1;
+          }
+          if (ttid == 0) s_cmax[0] = cmx;
+          cb ^= 1;
+          full = false;
+        }
+        if (pst && it < 256) atomicMax(pst + it * 8 + 6, globaltimer());
       }
-      if (pst && it < 256) atomicMax(pst + it * 8 + 6, globaltimer());
+      if (ra && ttid == 0) {  // the loop state for the run-ahead warps (they skipped the finish)
+        s_tail[0] = stop ? 1 : 0;
+        s_tail[1] = exhausted ? 1 : 0;
+        s_tail[2] = t_upd;
+        s_tail[3] = cb;
+        s_tail[4] = full ? 1 : 0;
+      }
     }
     __syncthreads();
+    if (ra_role) {
+      stop = s_tail[0] != 0;
+      exhausted = s_tail[1] != 0;
+      t_upd = s_tail[2];
+      cb = s_tail[3];
+      full = s_tail[4] != 0;
+    }
     if (pst && it < 256) atomicMax(pst + it * 8 + 7, globaltimer());
     if (stop) break;
     g0 += pass_tiles;
@@ -1653,7 +1714,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   // ---- teardown ----
   if (resident && warp == kProducerWarp && lane == 0) {
     // the prefetched tiles of the pass that does not run: let their copies land before exit
-    for (int j = 0; j < npre; ++j) {
+    // (npre, plus the tiles issued ahead in the last tail: only each slot's latest tile — an earlier
+    // occupant's phase completed before its slot was reused, and its parity would alias)
+    for (int j = max(0, issued - RS); j < issued; ++j) {
       const int g = g0 + last_pass_tiles + j;
       mbar_wait(full_raw + g % RS, (g / RS) & 1);
     }
