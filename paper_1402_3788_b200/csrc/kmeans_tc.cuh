@@ -113,8 +113,11 @@ __host__ __device__ constexpr int tc_pdelta_bytes() {
 
 template <int MP, int KP, int TR>
 struct TcBudget {
+// A buffers per transform group with A in TMEM: 6 at KP = 16 (12 × 32 + 8 score buffers × 16 = 512
+// TMEM columns; deeper run-ahead in the tail: 42.8 → 42.1 µs per steady pass at cfg3), 4 at KP = 32
+// (so the score ring keeps 8 buffers and three epilogue groups)
 #ifndef KM_TS_ABUF
-#define KM_TS_ABUF 4
+#define KM_TS_ABUF (KP <= 16 ? 6 : 4)
 #endif
   // A buffers: per transform group (a group owns buffers g mod a); in TMEM they are cheap
   static constexpr int a = (tc_a_in_tmem<KP, TR>() ? KM_TS_ABUF : 2) * kTransformGroups;
