@@ -1424,13 +1424,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
     if (pst && (it == 100 || it == 101 || it == 150))
       a.dbg_times[6144 + (it == 100 ? 0 : it == 101 ? 300 : 600) + blockIdx.x * 2 + 1] = (long long)globaltimer();
-    // Run-ahead (resident, next pass not heavy, not the final pass of an exhausted run): while the
-    // other warps run the tail below (Δ flush, grid barrier, finish, next B operand), the transform
-    // groups convert the next pass's first AS tiles (already prefetched) into the A buffers and the
-    // producer streams the next tiles into the raw slots this frees — the HBM stream and the
-    // transform no longer stop for the tail.  Only tile data moves ahead; nothing depends on C.
+    // Run-ahead (resident, not the final pass of an exhausted run): while the other warps run the
+    // tail below (Δ flush, grid barrier, finish, next B operand), the transform groups convert the
+    // next pass's first AS tiles (already prefetched) into the A buffers and — unless the next pass
+    // is heavy (its epilogue, not the transform, releases the raw slots) — the producer streams
+    // the next tiles into the slots this frees: the HBM stream and the transform no longer stop
+    // for the tail.  Only tile data moves ahead; nothing depends on C.
     __syncthreads();  // s_heavy of the next pass, visible to every role
-    const bool ra = KM_RUN_AHEAD && resident && !exhausted && s_heavy == 0 && my_tiles > 0;
+    const bool ra = KM_RUN_AHEAD && resident && !exhausted && my_tiles > 0;
+    const bool hv_next = s_heavy != 0;
     const bool ra_role = ra && (warp < kTransformWarps || warp == kProducerWarp);
     // tail threads: all of them, or (run-ahead) every warp but the transform groups and the producer
     const int ttid = !ra ? tid : warp < kProducerWarp ? tid - kTransformWarps * 32 : tid - (kTransformWarps + 1) * 32;
@@ -1444,9 +1446,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
     pre_done = 0;
     if (ra_role) {
       const int gn = g0 + pass_tiles;        // first tile of the next pass
-      const int pre_n = min(AS, my_tiles);   // transformed ahead (≤ npre: already prefetched)
+      // transformed ahead: tiles the producer has issued or issues now (heavy next pass: no slot is
+      // released before its epilogue, so only the npre prefetched tiles)
+      const int pre_n = min(AS, hv_next ? npre : my_tiles);
       if (warp == kProducerWarp) {
-        if (lane == 0) {  // refill the slots the run-ahead transform releases
+        if (lane == 0 && !hv_next) {  // refill the slots the run-ahead transform releases
           const int upto = min(npre + pre_n, my_tiles);
           for (int j = issued; j < upto; ++j) issue(gn + j, j);
           issued = max(issued, upto);
@@ -1454,7 +1458,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       } else {
         for (int j = ((tg - gn) % kTransformGroups + kTransformGroups) % kTransformGroups; j < pre_n;
              j += kTransformGroups)
-          transform_tile(gn + j, j, false);
+          transform_tile(gn + j, j, hv_next);
       }
       pre_done = pre_n;
     } else {
