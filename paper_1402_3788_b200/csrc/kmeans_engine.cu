@@ -454,8 +454,8 @@ static int launch_tc(km_engine* e, bool full, bool gated, bool fuse = false, boo
           ++cnt;
         }
         if (cnt)
-          fprintf(f, "resident passes 20..%d (ns after CTA0 start): main %.0f recheck %.0f flush %.0f arrive %.0f "
-                  "divide %.0f conv %.0f prep %.0f\n", 20 + cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
+          fprintf(f, "resident passes 20..%d (ns after CTA0 start): main %.0f recheck %.0f flush %.0f barrier-passed %.0f "
+                  "finish %.0f conv %.0f prep %.0f\n", 20 + cnt, acc[1] / cnt, acc[2] / cnt, acc[3] / cnt,
                   acc[4] / cnt, acc[5] / cnt, acc[6] / cnt, acc[7] / cnt);
       }
       fprintf(f, "----\n");

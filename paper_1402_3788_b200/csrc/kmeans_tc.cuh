@@ -878,7 +878,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
   int last_pass_tiles = my_tiles;
 
   // tuning only: per-pass phase ends (globaltimer, max over CTAs) of the resident loop
-  unsigned long long* pst = (KM_TC_TUNING && a.dbg_times != nullptr && resident && tid == 0)
+  unsigned long long* pst = (KM_TC_TUNING && a.dbg_times != nullptr && resident && tid == kTransformWarps * 32)
                                 ? reinterpret_cast<unsigned long long*>(a.dbg_times + 4096) : nullptr;
   for (int it = 0;; ++it) {
     // tiles of this pass (resident skip_first: the labels and their sums come from a separate
@@ -1526,13 +1526,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) 
       // 0's gpu-scope fence by the CTA barrier, so one fence per CTA (not one per thread) releases them
       tsync();
       if (pst && it < 256) atomicMax(pst + it * 8 + 3, globaltimer());
-      if (pst && it < 256) atomicMax(pst + it * 8 + 4, globaltimer());
       if (ttid == 0) {
         __threadfence();
         atomicAdd(a.grid_sync, 1u);
         grid_spin(a.grid_sync, (unsigned int)(it + 1) * gridDim.x);
       }
       tsync();
+      if (pst && it < 256) atomicMax(pst + it * 8 + 4, globaltimer());  // (tuning: barrier passed)
       if (a.xch_peers != nullptr) {
         // ---- row-sharded multi-GPU: exchange this iteration's Δ with every rank over NVLink ----
         // CTA 0 pushes the rank's complete Δ (the local grid barrier has passed) into slot
