@@ -732,13 +732,31 @@ static __device__ __forceinline__ void delta_rows_smem(const float* __restrict__
   }
 }
 
+// Epilogue warpgroups of an instantiation: four for the cfg5 shape (m = 25, K = 64, fp32 points),
+// whose 64-score epilogue bounds the pass (69.6 → 68.4 µs per 2M-point pass; 28 warps at 72
+// registers: that instantiation spills ~0.2 KB, the m-bucket ones would spill ~1 KB), three elsewhere.
+template <int MT, int KP, bool X64>
+__host__ __device__ constexpr int tc_epi_groups() { return (MT == 25 && KP == 64 && !X64) ? 4 : kEpiGroups; }
+template <int MT, int KP, bool X64>
+__host__ __device__ constexpr int tc_threads() { return (kTransformWarps + 4 * tc_epi_groups<MT, KP, X64>() + 4) * 32; }
+
 // X64: fp64 points — the pass streams their fp32 shadow (a.x), the exact rows (a.x64) feed the
 // recheck and the Δ; a separate instantiation so the fp32 kernels carry none of it
 template <int MT, int KP, bool PRE, bool X64>
-__global__ void __launch_bounds__(kThreadsTC, 1) lloyd_pass_tc_kernel(TcArgs a) {
+__global__ void __launch_bounds__(tc_threads<MT, KP, X64>(), 1) lloyd_pass_tc_kernel(TcArgs a) {
+  // this instantiation's warp roles (they shadow the defaults above)
+  constexpr int kEpiGroups = tc_epi_groups<MT, KP, X64>();
+  constexpr int kEpiWarps = 4 * kEpiGroups;
+  constexpr int kProducerWarp = kTransformWarps + kEpiWarps;
+  constexpr int kMmaWarp = kProducerWarp + 1;
+  constexpr int kRecheckWarp = kMmaWarp + kMmaWarps;
+  constexpr int kThreadsTC = (kRecheckWarp + 1) * 32;
+  constexpr int kTailThreads = kThreadsTC - (kTransformWarps + 1) * 32;
   static_assert(kThreadsTC == (kTransformWarps + kEpiWarps + 4) * 32, "warp-role layout");
+  static_assert(kThreadsTC == tc_threads<MT, KP, X64>(), "launch bounds");
   const double* __restrict__ x64p = X64 ? a.x64 : nullptr;
   constexpr int MP = MT > 0 ? MT : -MT;
+  static_assert(!tc_pdelta<MP, KP>() || kEpiWarps == tc::kEpiWarps, "private Δ is sized for the default roles");
   if (a.gate && (a.st->done || a.st->need_host)) return;
   using L = TcLayout<MP>;
   constexpr int TR = TcStages<MP, KP>::TR;  // points per tile
@@ -1769,7 +1787,7 @@ inline int launch_t(const TcArgs& a, int num_sms, size_t smem_optin, cudaStream_
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)num_sms));  // one persistent CTA/SM
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kThreadsTC);
+  cfg.blockDim = dim3(tc_threads<MT, KP, X64>());
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
