@@ -595,7 +595,8 @@ __device__ __forceinline__ int exact_candidates(const T* __restrict__ gx, int m,
 //   pass t → flush the CTA's Δ into the running totals → grid barrier → every CTA
 //   computes C_{t+1} = S/N, the empty count, the congruence test and its own copy of
 //   the B operand (bit-identical in every CTA) → pass t+1.  The TMA producer streams
-//   the first tiles of pass t+1 while the tail, the barrier and the finish run.  Stops
+//   the first tiles of pass t+1, and the transform groups convert them (run-ahead), while
+//   the other warps run the tail, the barrier and the finish.  Stops
 //   on convergence, after the final assign pass of an exhausted run, or on empty
 //   clusters (the host repairs them and relaunches).
 // Exact incremental update of the per-cluster fixed-point sums for the changed points of one warp
@@ -1432,7 +1433,7 @@ __global__ void __launch_bounds__(tc_threads<MT, KP, X64>(), 1) lloyd_pass_tc_ke
       __syncwarp();
       if (lane == 0) atomicAdd(s_qn + 1, 1u);  // this epilogue warp has queued everything of the pass
     }
-    // ===================== tail (all warps) =====================
+    // ===================== tail =====================
     tc_fence_before();
     __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
     if (tid == 0 && pass_tiles > 0) {  // the next pass is heavy if this one changed > 1/256 of the CTA's points
