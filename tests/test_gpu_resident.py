@@ -130,3 +130,22 @@ def test_sharded_nccl_world1_equals_resident():
         assert np.array_equal(got.centers, want[0])
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("max_iters,tol", [(1000, 0.0), (1000, 1e-3), (1000, 1e-2), (7, 0.0), (8, 0.0)])
+def test_run_ahead_stop_points_vs_oracle(max_iters, tol):
+    """n ≥ 500k: split first pass, then the resident loop whose tails run ahead into the next pass
+    (transform + raw-slot refill).  Stopping right after such a tail — convergence at tol = 0 or at
+    a coarse tol, or an exhausted run's final pass — must leave the result exactly the reference's
+    (and the launch must end cleanly: the teardown waits for each raw slot's latest copy only)."""
+    from oracle import oracle
+    from paper_1402_3788_b200.datasets import generate_synthetic_array
+
+    x = generate_synthetic_array(600_000, 25, 16, seed=8, dtype=np.float32)
+    c0 = x[:16].astype(np.float64)
+    centers, counts, labels, it, conv, st = fit(x, c0, max_iters, tol, resident=True)
+    want = oracle.lloyd(x.astype(np.float64), c0, max_iters=max_iters, tol=tol, n_workers=16)
+    assert it == want["iterations"] and conv == want["converged"]
+    assert np.array_equal(labels, want["labels"]) and np.array_equal(counts, want["counts"])
+    rel = np.max(np.abs(centers - want["centers"]) / np.maximum(np.abs(want["centers"]), 1.0))
+    assert rel <= 1e-12
