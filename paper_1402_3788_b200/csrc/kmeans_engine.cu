@@ -1228,7 +1228,7 @@ static int lloyd_resident(km_engine* e, const double* c0, int max_iters, double 
   trace();
   if (!resume) {
     // C0: in the begin kernel's parameters when it fits, else one pinned H2D copy
-    C0Inline c0p;  // (by-value launch parameter; only the first k·m entries are read)
+    C0Inline c0p{};  // (by-value launch parameter; only the first k·m entries are read)
     const bool inl = km <= (size_t)kC0Inline;
     if (inl) {
       std::memcpy(c0p.v, c0, 8 * km);
