@@ -57,6 +57,9 @@ constexpr long long kChangeFlag = 1ll << 61;
 #ifndef KM_HEAVY_PASSES
 #define KM_HEAVY_PASSES 1
 #endif
+#ifndef KM_HEAVY_DIV
+#define KM_HEAVY_DIV 256  // a pass is heavy when its predecessor changed more than 1/KM_HEAVY_DIV of the CTA's points
+#endif
 #ifndef KM_QUEUE_CHANGES
 #define KM_QUEUE_CHANGES 0
 #endif
@@ -1437,7 +1440,7 @@ __global__ void __launch_bounds__(tc_threads<MT, KP, X64>(), 1) lloyd_pass_tc_ke
     tc_fence_before();
     __syncthreads();  // every role done with this pass: the CTA's Δ is complete in s_acc
     if (tid == 0 && pass_tiles > 0) {  // the next pass is heavy if this one changed > 1/256 of the CTA's points
-      s_heavy = KM_HEAVY_PASSES && !no_sums && !x64p && s_pass_changes * 256u > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
+      s_heavy = KM_HEAVY_PASSES && !no_sums && !x64p && s_pass_changes * (unsigned int)KM_HEAVY_DIV > (unsigned int)pass_tiles * kTileRows ? 1 : 0;
       s_pass_changes = 0u;
     }
     if (pst && it < 256) atomicMax(pst + it * 8 + 1, globaltimer());
